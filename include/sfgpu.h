@@ -1,0 +1,167 @@
+/* sfgpu.h -- C-ABI of the B200-native Sparse Fusion executor (libsfgpu.so).
+ *
+ * The reference (header-only C++20, namespace sparsefuse) has no C ABI; its
+ * inspector/executor API is the interface this library replaces.  Each entry
+ * point names the reference function it stands in for.  Plain pointers and
+ * sizes only; every call returns an sfg_status.  The C++ mirror of the
+ * reference API (include/sparsefuse_b200.hpp) and the Python bindings
+ * (paper_2111_12238_b200/abi.py) sit on top of this header.
+ *
+ * Threading / ownership (kernels.hpp:409-427): a plan owns
+ * all device buffers of one KernelState; one execution at a time per plan;
+ * a plan is bound to the CUDA device current at creation.  Executions are
+ * asynchronous on the plan's stream; sfg_synchronize() (or any call that
+ * reads results back) surfaces numeric breakdown as SFG_ERR_FACTORIZATION
+ * with the failing index (types.hpp:17-26).
+ *
+ * Combos (kernels.hpp:53-68):
+ *   1 sptrsv-sptrsv  x = inv(L)*b; z = inv(L)*x      (nsys >= 1)
+ *   4 sptrsv-spmv    y = inv(L)*b; z = A*y
+ *   5 spic0-sptrsv   L*L' ~= A; y = inv(L)*b
+ *   6 spilu0-sptrsv  LU ~= A; y = inv(L)*b  (unit L)
+ *   7 dscal-spic0    L*L' ~= D*A*D'
+ *   8 sptrsv-sptrsvT z = inv(L)*b; x = inv(L')*z     (nsys >= 1; BASELINE
+ *     config 5 -- not in the reference, whose level_info rejects descending
+ *     edges, dag.hpp:204-205)
+ */
+#ifndef SFGPU_H
+#define SFGPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  SFG_OK = 0,
+  SFG_ERR_FACTORIZATION = 1,    /* sparsefuse::FactorizationError (types.hpp:17-26) */
+  SFG_ERR_INVALID_MATRIX = 2,   /* sparsefuse::InvalidMatrixError (types.hpp:28-31) */
+  SFG_ERR_INVALID_ARGUMENT = 3, /* std::invalid_argument (kernels.hpp:72, msp.hpp:828-829) */
+  SFG_ERR_CUDA = 4,             /* CUDA runtime failure (no reference analogue) */
+  SFG_ERR_LOGIC = 5,            /* std::logic_error (executor.hpp:398-399) */
+  SFG_ERR_NO_DEVICE = 6         /* no CUDA device: the library never falls back to the CPU */
+} sfg_status;
+
+/* Factorization error kinds reported by sfg_last_error (same numbering as
+ * oracle/sf_oracle.h). */
+enum {
+  SFG_FERR_ZERO_DIAG_SOLVE = 1, /* "zero diagonal in triangular solve" kernels.hpp:178-179,207-208 */
+  SFG_FERR_NONPOS_PIVOT = 2,    /* "non-positive pivot" kernels.hpp:235-237 */
+  SFG_FERR_ZERO_PIVOT = 3,      /* "zero pivot" kernels.hpp:260-261 */
+  SFG_FERR_INVALID_MATRIX = 4,  /* lower_triangle / build_lower_rows: matrix.hpp:98-128, kernels.hpp:97-99 */
+  SFG_FERR_ZERO_DIAG_SCALE = 5  /* scaling_vector "zero diagonal" kernels.hpp:304-305 */
+};
+
+typedef struct sfg_plan sfg_plan;
+
+/* Library / device ------------------------------------------------------- */
+/* Returns SFG_OK when a CUDA device is usable; SFG_ERR_NO_DEVICE otherwise. */
+sfg_status sfg_device_check(int32_t* device_count, int32_t* sm_count);
+const char* sfg_version(void);
+
+/* Plan lifetime (replaces make_state, kernels.hpp:429-495) ----------------
+ * M: square CSC matrix (n, colptr[n+1], rowidx[nnz], values), host memory.
+ * nsys: number of independent systems sharing M's pattern (> 1 only for
+ *   combos 1 and 8); `values` then holds nsys*nnz doubles, system-major.
+ * vin: nsys*n doubles (system-major) or NULL, in which case system s uses
+ *   gen_vector(n, seed + s) (fixtures.hpp:148-155; seed + 0 for nsys == 1,
+ *   i.e. exactly make_state's vector).  Ignored for combo 7.
+ * Storage conversions (lower_triangle, to_csr, build_lower_rows,
+ * find_diag_positions, the DSCAL vector) run on the GPU. */
+sfg_status sfg_plan_create(int32_t combo, int32_t n, const int32_t* colptr,
+                           const int32_t* rowidx, const double* values,
+                           int32_t nsys, const double* vin, uint64_t seed,
+                           sfg_plan** out);
+sfg_status sfg_plan_destroy(sfg_plan* plan);
+/* Use the caller's cudaStream_t (NULL = the plan's own stream). */
+sfg_status sfg_plan_set_stream(sfg_plan* plan, void* cuda_stream);
+sfg_status sfg_plan_info(const sfg_plan* plan, int32_t* combo, int32_t* n,
+                         int32_t* nsys, int64_t* nnz_factor,
+                         int64_t* output_len_per_system);
+/* Replace the input vectors (st.vin = ...): nsys*n doubles, system-major,
+ * host memory (pinned or pageable).  Asynchronous on the plan stream. */
+sfg_status sfg_set_vin(sfg_plan* plan, const double* vin_host);
+
+/* Inspector (replaces build_g1/build_g2/inter_dag/joint_dag/level_info/
+ * compute_reuse, dag.hpp:150-431, and msp + compile_schedule,
+ * msp.hpp:825-1082 / executor.hpp:235-268) --------------------------------
+ * sfg_inspect builds, on the GPU, the executor's task DAG levels and the
+ * dependency-ordered ticket list (a linear extension of the joint DAG, grouped
+ * by wavefront).  Must be called once before executing. */
+sfg_status sfg_inspect(sfg_plan* plan);
+/* DAG export for parity: which = 1 (G1, build_g1), 2 (G2, build_g2),
+ * 3 (joint_dag(G1, G2, F)).  Two-phase: call with NULL arrays to get sizes. */
+sfg_status sfg_get_dag(sfg_plan* plan, int32_t which, int32_t* nvert,
+                       int64_t* nedges, int32_t* succptr, int32_t* succ,
+                       int64_t* cost);
+/* inter_dag F (dag.hpp:279-317). Two-phase like sfg_get_dag. */
+sfg_status sfg_get_interdep(sfg_plan* plan, int32_t* nrows, int32_t* ncols,
+                            int64_t* nnz, int32_t* rowptr, int32_t* colidx);
+/* level_info of G1 / G2 / joint (dag.hpp:197-218), computed on the GPU. */
+sfg_status sfg_get_levels(sfg_plan* plan, int32_t which, int32_t* level,
+                          int32_t* height, int32_t* slack,
+                          int32_t* critical_path);
+/* compute_reuse (dag.hpp:398-431). */
+sfg_status sfg_compute_reuse(sfg_plan* plan, double* reuse);
+/* The fused schedule built by sfg_inspect: tickets in execution order as
+ * (tag, iter) pairs and the wavefront boundaries.  Two-phase. */
+sfg_status sfg_get_schedule(sfg_plan* plan, int64_t* nentries,
+                            uint8_t* tags, int32_t* iters, int32_t* nwaves,
+                            int64_t* wave_ptr);
+
+/* Executor (replaces execute_fused / execute_unfused, executor.hpp:325-461)
+ * Asynchronous on the plan stream. */
+sfg_status sfg_execute_fused(sfg_plan* plan);
+/* Unfused comparator: kernel 1 in one launch, kernel 2 in a second launch. */
+sfg_status sfg_execute_unfused(sfg_plan* plan);
+/* Waits for the plan stream; returns SFG_ERR_FACTORIZATION on breakdown. */
+sfg_status sfg_synchronize(sfg_plan* plan);
+/* collect_outputs (kernels.hpp:585-608) for every system, system-major,
+ * into host memory; synchronizes.  cap in doubles. */
+sfg_status sfg_collect_outputs(sfg_plan* plan, double* out_host, int64_t cap);
+/* Device pointer of the interleaved output arrays for zero-copy consumers:
+ * which = 0 vmid / fac, 1 vout / dvec.  Valid until the next execution. */
+sfg_status sfg_device_output(sfg_plan* plan, int32_t which, void** dptr,
+                             int64_t* count);
+/* Last error of the plan: status, factorization kind and failing index,
+ * message as the reference would print it. */
+sfg_status sfg_last_error(const sfg_plan* plan, int32_t* ferr_kind,
+                          int32_t* index, char* msg, int32_t msg_len);
+/* Kernel launches issued by this plan since creation (bench accounting). */
+int64_t sfg_launch_count(const sfg_plan* plan);
+/* Device-side duration in ms of the last sfg_execute_* call, from CUDA
+ * events recorded on the plan stream around the executor kernels (waits for
+ * completion).  kernel_ms (optional) receives the time of the dominant
+ * executor kernel alone. */
+sfg_status sfg_last_exec_ms(sfg_plan* plan, float* total_ms, float* kernel_ms);
+
+/* Fixtures (replaces fixtures.hpp generators + the BASELINE configs) -------
+ * Generated matrices are returned through an opaque handle. */
+typedef struct sfg_matrix sfg_matrix;
+/* kind: 0 gen_grid_laplacian(a) (fixtures.hpp:49-91)
+ *       1 gen_banded_spd(a, b, seed) (fixtures.hpp:97-141)
+ *      10 BASELINE config 1: 2-D 5-pt Laplacian, a x a grid, natural order
+ *      11 config 2: 3-D 7-pt Laplacian a^3, diagonal 6.01
+ *      12 config 3: 3-D 7-pt convection-diffusion a^3, beta ~ U[0,0.5] (seed)
+ *      13 config 4: random symmetric band, n = a, half-width b, 8 draws/row
+ *      14 config 5: 3-D 27-pt stencil a^3, diagonal 26.5, off -1 */
+sfg_status sfg_matrix_gen(int32_t kind, int32_t a, int32_t b, uint64_t seed,
+                          sfg_matrix** out);
+sfg_status sfg_matrix_dims(const sfg_matrix* m, int32_t* n, int64_t* nnz);
+sfg_status sfg_matrix_copy(const sfg_matrix* m, int32_t* colptr,
+                           int32_t* rowidx, double* values);
+sfg_status sfg_matrix_free(sfg_matrix* m);
+/* Config 5 per-system values: system s adds delta_s,i ~ U[0, 0.1]
+ * (mt19937_64 seeded seed0 + s) to diagonal entry i.  out: nsys*nnz doubles. */
+sfg_status sfg_matrix_perturb_diag(const sfg_matrix* m, int32_t nsys,
+                                   uint64_t seed0, double* out);
+/* gen_vector (fixtures.hpp:148-155). */
+sfg_status sfg_gen_vector(int32_t n, uint64_t seed, double* out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif

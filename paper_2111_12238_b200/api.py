@@ -1,0 +1,408 @@
+"""Host-side mirror of the reference inspector/executor API (namespace
+``sparsefuse``, proj/include/sparsefuse/*.hpp) over the C-ABI.
+
+Same names, argument meaning and error behaviour as the reference, so code
+written against it ports line for line::
+
+    st  = make_state(5, M, seed=7)              # kernels.hpp:429
+    g1  = build_g1(st); g2 = build_g2(st)       # dag.hpp:319,339
+    f   = inter_dag(st)                         # dag.hpp:279
+    j   = joint_dag(st)                         # dag.hpp:222 (built on the GPU)
+    li  = level_info(st, 3)                     # dag.hpp:197
+    sch = make_fused_schedule(st)               # msp + compile_schedule
+    execute_fused(sch, st)                      # executor.hpp:395
+    out = collect_outputs(st)                   # kernels.hpp:585
+
+Numeric breakdown raises ``FactorizationError`` with the failing index
+(types.hpp:17-26); invalid input raises ``InvalidMatrixError``.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import abi
+from .abi import f64p, i32p, i64p, ptr, u8p
+
+# kernels.hpp:53-68 plus combo 8 (forward L, backward L^T; BASELINE config 5)
+COMBOS = {
+    1: ("sptrsv-sptrsv", "x = inv(L)*y; z = inv(L)*x"),
+    4: ("sptrsv-spmv", "y = inv(L)*x; z = A*y"),
+    5: ("spic0-sptrsv", "L*L' ~= A; y = inv(L)*x"),
+    6: ("spilu0-sptrsv", "LU ~= A; y = inv(L)*x"),
+    7: ("dscal-spic0", "L*L' ~= D*A*D'"),
+    8: ("sptrsv-sptrsvT", "z = inv(L)*b; x = inv(L')*z"),
+}
+
+
+class FactorizationError(RuntimeError):
+    """sparsefuse::FactorizationError (types.hpp:17-26)."""
+
+    def __init__(self, what: str, index: int, kind: int = 0):
+        super().__init__(what)
+        self.index = index
+        self.kind = kind
+
+
+class InvalidMatrixError(RuntimeError):
+    """sparsefuse::InvalidMatrixError (types.hpp:28-31)."""
+
+
+class NoDeviceError(RuntimeError):
+    """No CUDA device: this library has no CPU fallback by design."""
+
+
+@dataclass
+class CscMatrix:
+    """CscMatrix (matrix.hpp:18-26)."""
+
+    n: int
+    colptr: np.ndarray
+    rowidx: np.ndarray
+    values: np.ndarray
+
+    @property
+    def nnz(self) -> int:
+        return int(self.colptr[-1])
+
+
+@dataclass
+class DepDag:
+    """DepDag (dag.hpp:17-30)."""
+
+    nvert: int
+    succptr: np.ndarray
+    succ: np.ndarray
+    cost: np.ndarray
+
+    def nedges(self) -> int:
+        return int(self.succptr[-1]) if len(self.succptr) else 0
+
+
+@dataclass
+class InterDep:
+    """InterDep F (dag.hpp:34-41)."""
+
+    nrows: int
+    ncols: int
+    rowptr: np.ndarray
+    colidx: np.ndarray
+
+
+@dataclass
+class LevelInfo:
+    """LevelInfo (dag.hpp:43-48)."""
+
+    level: np.ndarray
+    height: np.ndarray
+    slack: np.ndarray
+    critical_path: int
+
+
+@dataclass
+class FusedSchedule:
+    """The GPU-built fused schedule: entries (tag, iter) in ticket order,
+    grouped into wavefronts (the s-partition analogue) by ``wave_ptr``."""
+
+    tags: np.ndarray
+    iters: np.ndarray
+    wave_ptr: np.ndarray
+
+    def nspartitions(self) -> int:
+        return len(self.wave_ptr) - 1
+
+
+def _raise(L, h, st: int, what: str):
+    if st == abi.SFG_OK:
+        return
+    kind = C.c_int32(0)
+    idx = C.c_int32(-1)
+    msg = C.create_string_buffer(512)
+    if h:
+        L.sfg_last_error(h, C.byref(kind), C.byref(idx), msg, 512)
+    text = msg.value.decode() or what
+    if st == abi.SFG_ERR_FACTORIZATION:
+        raise FactorizationError(text, idx.value, kind.value)
+    if st == abi.SFG_ERR_INVALID_MATRIX:
+        raise InvalidMatrixError(text)
+    if st == abi.SFG_ERR_INVALID_ARGUMENT:
+        raise ValueError(text)
+    if st == abi.SFG_ERR_NO_DEVICE:
+        raise NoDeviceError("no CUDA device: sfgpu runs on sm_100a only (no CPU fallback)")
+    if st == abi.SFG_ERR_LOGIC:
+        raise RuntimeError(text)
+    raise RuntimeError(f"{what}: {text} (status {st})")
+
+
+class KernelState:
+    """A KernelState (kernels.hpp:409-427) resident in GPU memory."""
+
+    def __init__(self, combo: int, M: CscMatrix, seed: int = 7, nsys: int = 1,
+                 values: np.ndarray | None = None, vin: np.ndarray | None = None):
+        self.L = abi.load()
+        self.combo = combo
+        self.n = M.n
+        self.nsys = nsys
+        cp = np.ascontiguousarray(M.colptr, np.int32)
+        ri = np.ascontiguousarray(M.rowidx, np.int32)
+        va = np.ascontiguousarray(M.values if values is None else values, np.float64)
+        if values is not None and va.size != nsys * M.nnz:
+            raise ValueError("values must hold nsys * nnz doubles")
+        vi = None if vin is None else np.ascontiguousarray(vin, np.float64)
+        h = C.c_void_p()
+        st = self.L.sfg_plan_create(combo, M.n, ptr(cp, i32p), ptr(ri, i32p), ptr(va, f64p),
+                                    nsys, ptr(vi, f64p), seed, C.byref(h))
+        self.h = h.value
+        if st != abi.SFG_OK:
+            try:
+                _raise(self.L, self.h, st, "make_state")
+            finally:
+                self.close()
+        info = [C.c_int32(), C.c_int32(), C.c_int32(), C.c_int64(), C.c_int64()]
+        self.L.sfg_plan_info(self.h, *[C.byref(x) for x in info])
+        self.nnz_factor = info[3].value
+        self.output_len = info[4].value
+        self.inspected = False
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.L.sfg_plan_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _chk(self, st, what):
+        _raise(self.L, self.h, st, what)
+
+    # ---- inputs
+    def set_vin(self, vin: np.ndarray):
+        v = np.ascontiguousarray(vin, np.float64)
+        if v.size != self.n * self.nsys:
+            raise ValueError("vin must hold nsys * n doubles")
+        self._chk(self.L.sfg_set_vin(self.h, ptr(v, f64p)), "set_vin")
+
+    def set_stream(self, stream_handle: int | None):
+        self._chk(self.L.sfg_plan_set_stream(self.h, stream_handle or None), "set_stream")
+
+    # ---- inspector
+    def inspect(self):
+        self._chk(self.L.sfg_inspect(self.h), "inspect")
+        self.inspected = True
+        return self
+
+    def dag(self, which: int) -> DepDag:
+        nv = C.c_int32()
+        ne = C.c_int64()
+        self._chk(self.L.sfg_get_dag(self.h, which, C.byref(nv), C.byref(ne), None, None, None),
+                  "dag")
+        sp = np.empty(nv.value + 1, np.int32)
+        su = np.empty(max(ne.value, 1), np.int32)
+        co = np.empty(max(nv.value, 1), np.int64)
+        self._chk(self.L.sfg_get_dag(self.h, which, None, None, ptr(sp, i32p), ptr(su, i32p),
+                                     ptr(co, i64p)), "dag")
+        return DepDag(nv.value, sp, su[:ne.value], co[:nv.value])
+
+    def inter_dag(self) -> InterDep:
+        nr = C.c_int32()
+        nc = C.c_int32()
+        nnz = C.c_int64()
+        self._chk(self.L.sfg_get_interdep(self.h, C.byref(nr), C.byref(nc), C.byref(nnz), None,
+                                          None), "inter_dag")
+        rp = np.empty(nr.value + 1, np.int32)
+        ci = np.empty(max(nnz.value, 1), np.int32)
+        self._chk(self.L.sfg_get_interdep(self.h, None, None, None, ptr(rp, i32p),
+                                          ptr(ci, i32p)), "inter_dag")
+        return InterDep(nr.value, nc.value, rp, ci[:nnz.value])
+
+    def level_info(self, which: int) -> LevelInfo:
+        nv = self.n if which < 3 else 2 * self.n
+        lv = np.empty(max(nv, 1), np.int32)
+        ht = np.empty(max(nv, 1), np.int32)
+        sl = np.empty(max(nv, 1), np.int32)
+        P = C.c_int32()
+        self._chk(self.L.sfg_get_levels(self.h, which, ptr(lv, i32p), ptr(ht, i32p),
+                                        ptr(sl, i32p), C.byref(P)), "level_info")
+        return LevelInfo(lv[:nv], ht[:nv], sl[:nv], P.value)
+
+    def compute_reuse(self) -> float:
+        r = C.c_double()
+        self._chk(self.L.sfg_compute_reuse(self.h, C.byref(r)), "compute_reuse")
+        return r.value
+
+    def schedule(self) -> FusedSchedule:
+        ne = C.c_int64()
+        nw = C.c_int32()
+        self._chk(self.L.sfg_get_schedule(self.h, C.byref(ne), None, None, C.byref(nw), None),
+                  "schedule")
+        tags = np.empty(max(ne.value, 1), np.uint8)
+        iters = np.empty(max(ne.value, 1), np.int32)
+        wp = np.empty(nw.value + 1, np.int64)
+        self._chk(self.L.sfg_get_schedule(self.h, None, ptr(tags, u8p), ptr(iters, i32p), None,
+                                          ptr(wp, i64p)), "schedule")
+        return FusedSchedule(tags[:ne.value], iters[:ne.value], wp)
+
+    # ---- executor
+    def execute_fused(self, sync: bool = True):
+        if not self.inspected:
+            self.inspect()
+        self._chk(self.L.sfg_execute_fused(self.h), "execute_fused")
+        if sync:
+            self.synchronize()
+
+    def execute_unfused(self, sync: bool = True):
+        if not self.inspected:
+            self.inspect()
+        self._chk(self.L.sfg_execute_unfused(self.h), "execute_unfused")
+        if sync:
+            self.synchronize()
+
+    def synchronize(self):
+        self._chk(self.L.sfg_synchronize(self.h), "synchronize")
+
+    def collect_outputs(self, out: np.ndarray | None = None) -> np.ndarray:
+        """All systems' collect_outputs, concatenated system-major."""
+        need = self.output_len * self.nsys
+        if out is None:
+            out = np.empty(max(need, 1), np.float64)
+        self._chk(self.L.sfg_collect_outputs(self.h, ptr(out, f64p), out.size), "collect_outputs")
+        return out[:need]
+
+    def last_exec_ms(self):
+        tot = C.c_float()
+        ker = C.c_float()
+        self._chk(self.L.sfg_last_exec_ms(self.h, C.byref(tot), C.byref(ker)), "last_exec_ms")
+        return tot.value, ker.value
+
+    def launch_count(self) -> int:
+        return int(self.L.sfg_launch_count(self.h))
+
+    def device_output(self, which: int):
+        p = C.c_void_p()
+        cnt = C.c_int64()
+        self._chk(self.L.sfg_device_output(self.h, which, C.byref(p), C.byref(cnt)),
+                  "device_output")
+        return p.value, cnt.value
+
+
+# ---- free functions with the reference's names --------------------------------
+def make_state(combo: int, M: CscMatrix, seed: int = 7, **kw) -> KernelState:
+    """make_state (kernels.hpp:429-495); storage conversions run on the GPU."""
+    return KernelState(combo, M, seed, **kw)
+
+
+def build_g1(st: KernelState) -> DepDag:
+    return st.dag(1)
+
+
+def build_g2(st: KernelState) -> DepDag:
+    return st.dag(2)
+
+
+def inter_dag(st: KernelState) -> InterDep:
+    return st.inter_dag()
+
+
+def joint_dag(st: KernelState) -> DepDag:
+    return st.dag(3)
+
+
+def level_info(st: KernelState, which: int = 3) -> LevelInfo:
+    return st.level_info(which)
+
+
+def compute_reuse(st: KernelState) -> float:
+    return st.compute_reuse()
+
+
+def make_fused_schedule(st: KernelState) -> FusedSchedule:
+    """The GPU inspector (replaces msp + compile_schedule)."""
+    st.inspect()
+    return st.schedule()
+
+
+def execute_fused(sched: FusedSchedule | None, st: KernelState, nthreads: int | None = None):
+    """execute_fused (executor.hpp:395-461) on the GPU. ``nthreads`` is
+    accepted for signature parity and ignored (the GPU grid is sized to the
+    device)."""
+    st.execute_fused()
+
+
+def execute_unfused(st: KernelState):
+    st.execute_unfused()
+
+
+def reset(st: KernelState):
+    """reset (kernels.hpp:498-502): every execution re-initialises its
+    outputs on the device, so this is a no-op kept for API parity."""
+
+
+def collect_outputs(st: KernelState) -> np.ndarray:
+    return st.collect_outputs()
+
+
+def gen_vector(n: int, seed: int) -> np.ndarray:
+    """gen_vector (fixtures.hpp:148-155)."""
+    out = np.empty(max(n, 1), np.float64)
+    abi.load().sfg_gen_vector(n, seed, ptr(out, f64p))
+    return out[:n]
+
+
+def _matrix(kind: int, a: int, b: int = 0, seed: int = 0, nsys_perturb: int = 0,
+            seed0: int = 1000):
+    L = abi.load()
+    h = C.c_void_p()
+    if L.sfg_matrix_gen(kind, a, b, seed, C.byref(h)) != abi.SFG_OK:
+        raise ValueError("bad generator parameters")
+    try:
+        n = C.c_int32()
+        nnz = C.c_int64()
+        L.sfg_matrix_dims(h, C.byref(n), C.byref(nnz))
+        cp = np.empty(n.value + 1, np.int32)
+        ri = np.empty(max(nnz.value, 1), np.int32)
+        va = np.empty(max(nnz.value, 1), np.float64)
+        L.sfg_matrix_copy(h, ptr(cp, i32p), ptr(ri, i32p), ptr(va, f64p))
+        M = CscMatrix(n.value, cp, ri[:nnz.value], va[:nnz.value])
+        if nsys_perturb:
+            vals = np.empty(nsys_perturb * nnz.value, np.float64)
+            L.sfg_matrix_perturb_diag(h, nsys_perturb, seed0, ptr(vals, f64p))
+            return M, vals
+        return M
+    finally:
+        L.sfg_matrix_free(h)
+
+
+def gen_grid_laplacian(k: int) -> CscMatrix:
+    """gen_grid_laplacian (fixtures.hpp:49-91), ND-numbered."""
+    return _matrix(0, k)
+
+
+def gen_banded_spd(n: int, bw: int, seed: int) -> CscMatrix:
+    """gen_banded_spd (fixtures.hpp:97-141)."""
+    return _matrix(1, n, bw, seed)
+
+
+FULL_SIZE = {1: 512, 2: 64, 3: 96, 4: 1_000_000, 5: 128}
+
+
+def config_matrix(cfg: int, size: int | None = None, seed: int = 7,
+                  halfwidth: int = 2000) -> CscMatrix:
+    """BASELINE.json config matrices (full size by default):
+    1: 5-pt 2-D Laplacian 512^2   2: 7-pt 3-D Laplacian 64^3
+    3: 7-pt convection-diffusion 96^3   4: random band n=1e6, half-width 2000
+    5: 27-pt 3-D stencil 128^3."""
+    a = FULL_SIZE[cfg] if size is None else size
+    return _matrix(9 + cfg, a, halfwidth if cfg == 4 else 0, seed)
+
+
+def config5_systems(size: int | None = None, nsys: int = 8, seed0: int = 1000):
+    """Config 5: the 27-point stencil and nsys per-system value arrays
+    (system s adds delta ~ U[0, 0.1], mt19937_64(seed0 + s), to the diagonal).
+    Returns (M, values[nsys * nnz]); b_s = gen_vector(n, 7 + s)."""
+    a = FULL_SIZE[5] if size is None else size
+    return _matrix(14, a, 0, 0, nsys_perturb=nsys, seed0=seed0)

@@ -1,0 +1,122 @@
+// common.cuh -- device-side building blocks shared by the inspector and the
+// executor kernels (sm_100a only).
+//
+// Synchronisation model (replaces SpinBarrier + std::atomic claims of
+// executor.hpp:36-68,416-456).  Every value one task produces for another is
+// a 64-bit word that is reset to SENT (all-ones, a NaN no IEEE operation
+// produces from non-SENT operands) before the launch.  A consumer polls the
+// very word it needs with ld.relaxed.gpu until it is not SENT; the producer
+// writes it once with st.relaxed.gpu.  Because each polled word is its own
+// flag there is no separate flag array, no fence and no second L2 round trip
+// per dependency.  Work is claimed as warp-wide tickets from one global
+// counter in a topological order, so every task a warp waits on has already
+// been claimed by a running warp: sync-free and deadlock-free without
+// relying on CTA residency.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace sfg {
+
+constexpr unsigned long long SENT = 0xFFFFFFFFFFFFFFFFull;
+constexpr unsigned long long CANON_NAN = 0x7FF8000000000000ull;
+
+__device__ __forceinline__ unsigned long long ld_relaxed_u64(const void* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void st_relaxed_u64(void* p, unsigned long long v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+__device__ __forceinline__ int ld_relaxed_i32(const int* p) {
+  int v;
+  asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void st_relaxed_i32(int* p, int v) {
+  asm volatile("st.relaxed.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// Spin until *p != SENT; exponential nanosleep backoff keeps the pollers from
+// saturating the L2 slices the producers are writing to.
+__device__ __forceinline__ double poll_f64(const double* p) {
+  unsigned long long v = ld_relaxed_u64(p);
+  if (v != SENT)
+    return __longlong_as_double((long long)v);
+  unsigned ns = 20;
+  do {
+    __nanosleep(ns);
+    ns = ns < 160 ? ns * 2 : 160;
+    v = ld_relaxed_u64(p);
+  } while (v == SENT);
+  return __longlong_as_double((long long)v);
+}
+
+// Publish a value; a computed all-ones NaN (only possible from SENT-like NaN
+// inputs) is canonicalised so it can never be mistaken for "not ready".
+__device__ __forceinline__ void publish_f64(double* p, double v) {
+  unsigned long long b = (unsigned long long)__double_as_longlong(v);
+  if (b == SENT)
+    b = CANON_NAN;
+  st_relaxed_u64(p, b);
+}
+
+// Integer flavour for the inspector: 0 = not ready (levels are >= 1).
+__device__ __forceinline__ int poll_pos_i32(const int* p) {
+  int v = ld_relaxed_i32(p);
+  if (v > 0)
+    return v;
+  unsigned ns = 20;
+  do {
+    __nanosleep(ns);
+    ns = ns < 160 ? ns * 2 : 160;
+    v = ld_relaxed_i32(p);
+  } while (v <= 0);
+  return v;
+}
+
+// Heights use -1 as "not ready" (heights are >= 0).
+__device__ __forceinline__ int poll_nonneg_i32(const int* p) {
+  int v = ld_relaxed_i32(p);
+  if (v >= 0)
+    return v;
+  unsigned ns = 20;
+  do {
+    __nanosleep(ns);
+    ns = ns < 160 ? ns * 2 : 160;
+    v = ld_relaxed_i32(p);
+  } while (v < 0);
+  return v;
+}
+
+// Warp-granular ticket claim: lane 0 takes `per_warp` tickets, broadcast.
+__device__ __forceinline__ long long claim_tickets(unsigned long long* counter,
+                                                   int per_warp) {
+  unsigned long long base = 0;
+  if ((threadIdx.x & 31) == 0)
+    base = atomicAdd(counter, (unsigned long long)per_warp);
+  return (long long)__shfl_sync(0xffffffffu, base, 0);
+}
+
+// Error word: the minimum key over all failing tasks reproduces the first
+// failure of the sequential reference (run_sequential_reference runs every
+// kernel-1 iteration before kernel 2, ascending): key = kernel-1 (bit 62) |
+// sequential position of the detecting iteration (bits 31..61) | index.
+__device__ __forceinline__ void report_error(unsigned long long* word,
+                                             int kernel, int seq_pos,
+                                             int index) {
+  const unsigned long long key =
+      ((unsigned long long)(kernel - 1) << 62) |
+      ((unsigned long long)(unsigned)seq_pos << 31) | (unsigned)index;
+  atomicMin(word, key);
+}
+
+__device__ __forceinline__ double ldg_f64(const double* p) { return __ldg(p); }
+__device__ __forceinline__ int ldg_i32(const int* p) { return __ldg(p); }
+
+} // namespace sfg

@@ -1,0 +1,1298 @@
+// plan.cu -- the C-ABI (include/sfgpu.h): plan = a KernelState resident in
+// HBM plus its GPU-built schedule.  Mirrors make_state / build_g1 / build_g2
+// / inter_dag / joint_dag / level_info / compute_reuse / execute_fused /
+// execute_unfused / collect_outputs (kernels.hpp, dag.hpp, executor.hpp).
+#include "../../include/sfgpu.h"
+#include "common.cuh"
+#include "executor.cuh"
+#include "internal.hpp"
+
+#include <cub/device/device_scan.cuh>
+
+#include <algorithm>
+#include <cstring>
+#include <memory>
+#include <random>
+#include <string>
+#include <vector>
+
+using namespace sfg;
+
+struct sfg_plan {
+  int combo = 0;
+  int32_t n = 0;
+  int32_t nsys = 1;
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  cudaStream_t own_stream = nullptr;
+  int64_t launches = 0;
+  int64_t nnzM = 0, nnzL = 0, nnzF = 0; // M, lower(M), factor outputs
+  int64_t lower_count = 0;
+
+  DBuf<int32_t> m_ptr, m_idx; // M pattern (CSC)
+  DBuf<int32_t> lr_ptr, lr_idx;
+  DBuf<double> lr_val;
+  DBuf<int32_t> lt_ptr, lt_idx;
+  DBuf<double> lt_val;
+  DBuf<int32_t> ar_ptr, ar_idx, diag;
+  DBuf<double> ar_val;
+  DBuf<int32_t> lc_ptr, lc_idx, rv_ptr, rv_col, rv_pos;
+  DBuf<double> lc_val, dvec;
+  DBuf<double> vin, vmid, vout, fac, work, staging;
+
+  // schedule
+  bool inspected = false;
+  DBuf<int32_t> order;
+  int64_t ntickets = 0;
+  std::vector<int64_t> wave_ptr; // wavefront boundaries over tickets
+  int32_t seg2_start_wave = -1;  // first wave of the second ticket segment
+  DBuf<unsigned long long> counter, err;
+
+  // parity structures (lazy)
+  std::unique_ptr<DevDag> dags[3];
+  std::unique_ptr<DevDag> fdep;
+  DBuf<int32_t> lev[3], hgt[3], slk[3];
+  int32_t crit[3] = {0, 0, 0};
+  bool have_levels[3] = {false, false, false};
+
+  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  bool timed = false;
+
+  // last error
+  int32_t ferr_kind = 0, ferr_index = -1;
+  std::string msg;
+};
+
+namespace {
+
+struct LaunchScope {
+  int64_t* prev;
+  explicit LaunchScope(sfg_plan* p) : prev(g_launch_counter) { g_launch_counter = &p->launches; }
+  ~LaunchScope() { g_launch_counter = prev; }
+};
+
+struct DeviceScope {
+  int prev = 0;
+  explicit DeviceScope(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev)
+      cudaSetDevice(dev);
+  }
+  ~DeviceScope() {
+    int cur = 0;
+    cudaGetDevice(&cur);
+    if (cur != prev)
+      cudaSetDevice(prev);
+  }
+};
+
+sfg_status set_err(sfg_plan* p, sfg_status st, const std::string& m, int32_t kind = 0,
+                   int32_t index = -1) {
+  if (p) {
+    p->msg = m;
+    p->ferr_kind = kind;
+    p->ferr_index = index;
+  }
+  return st;
+}
+
+template <typename F> sfg_status guarded(sfg_plan* p, F&& f) {
+  try {
+    return f();
+  } catch (const InvalidMatrix& e) {
+    return set_err(p, SFG_ERR_INVALID_MATRIX, e.what(), SFG_FERR_INVALID_MATRIX, e.index);
+  } catch (const InvalidArgument& e) {
+    return set_err(p, SFG_ERR_INVALID_ARGUMENT, e.what());
+  } catch (const CudaError& e) {
+    return set_err(p, SFG_ERR_CUDA, e.what());
+  } catch (const std::bad_alloc&) {
+    return set_err(p, SFG_ERR_CUDA, "host allocation failed");
+  } catch (const std::exception& e) {
+    return set_err(p, SFG_ERR_LOGIC, e.what());
+  }
+}
+
+inline unsigned grid_for(int64_t work, int block = 256) {
+  int64_t g = (work + block - 1) / block;
+  const int64_t cap = (int64_t)sm_count() * 32;
+  if (g > cap)
+    g = cap;
+  return (unsigned)(g < 1 ? 1 : g);
+}
+
+template <typename T> void upload(DBuf<T>& d, const T* h, int64_t n, cudaStream_t s) {
+  d.alloc(n > 0 ? n : 1);
+  if (n > 0)
+    SFG_CUDA(cudaMemcpyAsync(d.p, h, sizeof(T) * (size_t)n, cudaMemcpyHostToDevice, s));
+}
+
+__global__ void compose_kernel(const int32_t* __restrict__ a, const int32_t* __restrict__ b,
+                               int64_t n, int32_t* __restrict__ out) {
+  // out[q] = a[b[q]]
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < n;
+       q += (int64_t)gridDim.x * blockDim.x)
+    out[q] = a[b[q]];
+}
+
+// LowerRowView from the CSR of L (diagonal last per row): drop each row's
+// last entry; row i shifts left by i (kernels.hpp:92-115).
+__global__ void rowview_kernel(const int32_t* __restrict__ csr_ptr,
+                               const int32_t* __restrict__ csr_idx,
+                               const int32_t* __restrict__ perm, int32_t n,
+                               int32_t* __restrict__ rv_ptr, int32_t* __restrict__ rv_col,
+                               int32_t* __restrict__ rv_pos) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i <= n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    rv_ptr[i] = csr_ptr[i] - (int32_t)i;
+    if (i < n)
+      for (int32_t q = csr_ptr[i]; q < csr_ptr[i + 1] - 1; ++q) {
+        rv_col[q - i] = csr_idx[q];
+        rv_pos[q - i] = perm[q];
+      }
+  }
+}
+
+__global__ void iota_i32_kernel(int32_t* a, int64_t n, int32_t base) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    a[i] = base + (int32_t)i;
+}
+
+// Edge-key generators for the parity DAGs (dag.hpp:150-192, 222-238,
+// 279-317).  Every entry of a compressed structure yields one key (u<<32|v)
+// or the all-ones "no edge" key.
+enum EdgeMode {
+  EM_ROWS_LOWER = 0, // CSR rows: (col, row) if col < row
+  EM_COLS_BELOW = 1, // CSC columns: (col, row) if row > col
+  EM_LT_REV = 2,     // L' rows (orig i): (n-1-j, n-1-i) if j > i
+  EM_SUCC = 3,       // generic successor CSR with offsets
+  EM_FDEP = 4        // F rows i: (col, off_v + i)
+};
+
+__global__ void edge_keys_kernel(const int32_t* __restrict__ ptr, const int32_t* __restrict__ idx,
+                                 int32_t nmajor, int mode, int32_t n, int32_t off_u,
+                                 int32_t off_v, uint64_t* __restrict__ keys) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int32_t base = ptr[0];
+  for (int64_t m = warp; m < nmajor; m += nwarps) {
+    for (int32_t p = ptr[m] + lane; p < ptr[m + 1]; p += 32) {
+      const int32_t x = idx[p];
+      uint64_t key = ~0ull;
+      int64_t u = -1, v = -1;
+      switch (mode) {
+      case EM_ROWS_LOWER:
+        if (x < m) {
+          u = x;
+          v = m;
+        }
+        break;
+      case EM_COLS_BELOW:
+        if (x > m) {
+          u = m;
+          v = x;
+        }
+        break;
+      case EM_LT_REV:
+        if (x > m) {
+          u = n - 1 - x;
+          v = n - 1 - m;
+        }
+        break;
+      case EM_SUCC:
+        u = m + off_u;
+        v = x + off_v;
+        break;
+      case EM_FDEP:
+        u = x;
+        v = off_v + m;
+        break;
+      }
+      if (u >= 0)
+        key = ((uint64_t)u << 32) | (uint64_t)v;
+      keys[p - base] = key;
+    }
+  }
+}
+
+enum CostKind {
+  CK_ROWNNZ = 0,   // max(1, ptr[i+1]-ptr[i])  (SpTRSV_CSR, SpMV/DSCAL_CSC)
+  CK_IC0 = 1,      // dag.hpp:128-140
+  CK_TRSV_CSC = 2, // 1 + row-view count
+  CK_ILU0 = 3,     // dag.hpp:92-105
+  CK_UNIT = 4,     // combo 6 G2: 1 + strictly-lower count
+  CK_LT_REV = 5    // combo 8 G2: cost[n-1-i] = max(1, L' row length)
+};
+
+__global__ void cost_kernel(int kind, int32_t n, const int32_t* __restrict__ ptr,
+                            const int32_t* __restrict__ idx, const int32_t* __restrict__ ptr2,
+                            const int32_t* __restrict__ aux1, const int32_t* __restrict__ aux2,
+                            int64_t* __restrict__ cost) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t c = 0;
+    switch (kind) {
+    case CK_ROWNNZ:
+      c = max((int64_t)1, (int64_t)(ptr[i + 1] - ptr[i]));
+      break;
+    case CK_IC0: { // ptr = lc_ptr, ptr2 = rv_ptr, aux1 = rv_col, aux2 = rv_pos
+      int64_t t = ptr[i + 1] - ptr[i];
+      for (int32_t q = ptr2[i]; q < ptr2[i + 1]; ++q)
+        t += ptr[aux1[q] + 1] - aux2[q];
+      c = max((int64_t)1, t);
+      break;
+    }
+    case CK_TRSV_CSC: // ptr2 = rv_ptr
+      c = 1 + ptr2[i + 1] - ptr2[i];
+      break;
+    case CK_ILU0: { // ptr/idx = A_csr, aux1 = diag
+      int64_t t = ptr[i + 1] - ptr[i];
+      for (int32_t p = ptr[i]; p < ptr[i + 1]; ++p) {
+        const int32_t k = idx[p];
+        if (k >= i)
+          break;
+        if (aux1[k] >= 0)
+          t += ptr[k + 1] - aux1[k] - 1;
+      }
+      c = max((int64_t)1, t);
+      break;
+    }
+    case CK_UNIT: {
+      int64_t t = 1;
+      for (int32_t p = ptr[i]; p < ptr[i + 1]; ++p) {
+        if (idx[p] >= i)
+          break;
+        ++t;
+      }
+      c = t;
+      break;
+    }
+    case CK_LT_REV:
+      cost[n - 1 - i] = max((int64_t)1, (int64_t)(ptr[i + 1] - ptr[i]));
+      continue;
+    }
+    cost[i] = c;
+  }
+}
+
+__global__ void fdep_fill_kernel(int combo, int32_t n, const int32_t* __restrict__ m_ptr,
+                                 const int32_t* __restrict__ rv_ptr,
+                                 const int32_t* __restrict__ rv_col,
+                                 const int32_t* __restrict__ rowptr, int32_t* __restrict__ colidx) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int32_t w = rowptr[i];
+    switch (combo) {
+    case 1:
+    case 6:
+      colidx[w] = (int32_t)i;
+      break;
+    case 8:
+      colidx[w] = n - 1 - (int32_t)i;
+      break;
+    case 4:
+      if (m_ptr[i] < m_ptr[i + 1])
+        colidx[w] = (int32_t)i;
+      break;
+    case 5:
+    case 7:
+      for (int32_t q = rv_ptr[i]; q < rv_ptr[i + 1]; ++q)
+        colidx[w++] = rv_col[q];
+      colidx[w] = (int32_t)i;
+      break;
+    }
+  }
+}
+
+__global__ void fdep_count_kernel(int combo, int32_t n, const int32_t* __restrict__ m_ptr,
+                                  const int32_t* __restrict__ rv_ptr, int32_t* __restrict__ cnt) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i <= n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    if (i == n) {
+      cnt[i] = 0;
+      continue;
+    }
+    int32_t c = 1;
+    if (combo == 4)
+      c = m_ptr[i] < m_ptr[i + 1] ? 1 : 0;
+    else if (combo == 5 || combo == 7)
+      c = rv_ptr[i + 1] - rv_ptr[i] + 1;
+    cnt[i] = c;
+  }
+}
+
+__global__ void collect_pair_kernel(const double* __restrict__ vmid, const double* __restrict__ vout,
+                                    int32_t n, int32_t nsys, double* __restrict__ out) {
+  const int64_t total = (int64_t)n * nsys;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = t / nsys;
+    const int32_t s = (int32_t)(t - i * nsys);
+    out[(int64_t)s * 2 * n + i] = vmid[t];
+    out[(int64_t)s * 2 * n + n + i] = vout[t];
+  }
+}
+
+bool pow2_upto32(int32_t v) { return v == 1 || v == 2 || v == 4 || v == 8 || v == 16 || v == 32; }
+
+void validate_csc(int32_t n, const int32_t* colptr, const int32_t* rowidx) {
+  if (n < 0)
+    throw InvalidMatrix("negative dimension", -1);
+  if (colptr[0] != 0)
+    throw InvalidMatrix("colptr[0] != 0", 0);
+  for (int32_t j = 0; j < n; ++j) {
+    if (colptr[j] > colptr[j + 1])
+      throw InvalidMatrix("colptr not non-decreasing", j);
+    for (int32_t p = colptr[j]; p < colptr[j + 1]; ++p) {
+      if (rowidx[p] < 0 || rowidx[p] >= n)
+        throw InvalidMatrix("row index out of range", j);
+      if (p > colptr[j] && rowidx[p - 1] >= rowidx[p])
+        throw InvalidMatrix("row indices not strictly increasing", j);
+    }
+  }
+}
+
+// Source positions (into M) -> interleaved values of all systems.
+void values_from(const DBuf<double>& mval, int64_t nnzM, int32_t nsys, const int32_t* src,
+                 int64_t nnz, DBuf<double>& out, cudaStream_t s) {
+  out.alloc((nnz > 0 ? nnz : 1) * nsys);
+  gather_values(mval.p, nnzM, src, nnz, nsys, out.p, s);
+}
+
+void build_plan(sfg_plan* P, const int32_t* colptr, const int32_t* rowidx,
+                const double* values, const double* vin_h, uint64_t seed) {
+  cudaStream_t s = P->stream;
+  const int32_t n = P->n, S = P->nsys;
+  const int64_t nnzM = colptr[n];
+  P->nnzM = nnzM;
+  int64_t lower = 0;
+  for (int32_t j = 0; j < n; ++j)
+    for (int32_t p = colptr[j]; p < colptr[j + 1]; ++p)
+      if (rowidx[p] >= j)
+        ++lower;
+  P->lower_count = lower;
+
+  upload(P->m_ptr, colptr, (int64_t)n + 1, s);
+  upload(P->m_idx, rowidx, nnzM, s);
+  DBuf<double> mval;
+  upload(mval, values, nnzM * S, s);
+
+  const int combo = P->combo;
+  if (combo == 1 || combo == 4 || combo == 8 || combo == 5 || combo == 7) {
+    // lower_triangle (matrix.hpp:98-128)
+    DBuf<int32_t> src;
+    P->nnzL = lower_triangle(P->m_ptr.p, P->m_idx.p, mval.p, nnzM, S, n, P->lc_ptr,
+                             P->lc_idx, src, s);
+    const int64_t nnzL = P->nnzL;
+    if (combo == 5 || combo == 7)
+      values_from(mval, nnzM, S, src.p, nnzL, P->lc_val, s);
+    // CSR of L: to_csr (matrix.hpp:66-86), rows ascending columns, diag last
+    DBuf<int32_t> csr_ptr((int64_t)n + 1), csr_idx(nnzL > 0 ? nnzL : 1),
+        perm(nnzL > 0 ? nnzL : 1), srcc(nnzL > 0 ? nnzL : 1);
+    transpose(P->lc_ptr.p, P->lc_idx.p, n, n, nnzL, csr_ptr.p, csr_idx.p, perm.p, s);
+    if (combo == 1 || combo == 4 || combo == 8) {
+      compose_kernel<<<grid_for(nnzL), 256, 0, s>>>(src.p, perm.p, nnzL, srcc.p);
+      count_launch();
+      values_from(mval, nnzM, S, srcc.p, nnzL, P->lr_val, s);
+      P->lr_ptr = std::move(csr_ptr);
+      P->lr_idx = std::move(csr_idx);
+    } else {
+      // LowerRowView (kernels.hpp:92-115): perm maps CSR entries to L_csc positions
+      P->rv_ptr.alloc((int64_t)n + 1);
+      const int64_t nrv = nnzL - n;
+      P->rv_col.alloc(nrv > 0 ? nrv : 1);
+      P->rv_pos.alloc(nrv > 0 ? nrv : 1);
+      rowview_kernel<<<grid_for((int64_t)n + 1), 256, 0, s>>>(csr_ptr.p, csr_idx.p, perm.p, n,
+                                                               P->rv_ptr.p, P->rv_col.p,
+                                                               P->rv_pos.p);
+      count_launch();
+    }
+    if (combo == 8) {
+      // L' rows = L columns reversed: strictly-lower entries by descending
+      // row, then the diagonal (the reference's P L^T P^T solve order)
+      P->lt_ptr.alloc((int64_t)n + 1);
+      SFG_CUDA(cudaMemcpyAsync(P->lt_ptr.p, P->lc_ptr.p, sizeof(int32_t) * ((size_t)n + 1),
+                               cudaMemcpyDeviceToDevice, s));
+      P->lt_idx.alloc(nnzL > 0 ? nnzL : 1);
+      DBuf<int32_t> rperm(nnzL > 0 ? nnzL : 1);
+      reverse_segments(P->lc_ptr.p, P->lc_idx.p, n, P->lt_idx.p, rperm.p, s);
+      compose_kernel<<<grid_for(nnzL), 256, 0, s>>>(src.p, rperm.p, nnzL, srcc.p);
+      count_launch();
+      values_from(mval, nnzM, S, srcc.p, nnzL, P->lt_val, s);
+    }
+    if (combo == 4) {
+      // CSR view of the CSC SpMV operand A = M (row gather, see executor.cu)
+      P->ar_ptr.alloc((int64_t)n + 1);
+      P->ar_idx.alloc(nnzM > 0 ? nnzM : 1);
+      DBuf<int32_t> aperm(nnzM > 0 ? nnzM : 1);
+      transpose(P->m_ptr.p, P->m_idx.p, n, n, nnzM, P->ar_ptr.p, P->ar_idx.p, aperm.p, s);
+      values_from(mval, nnzM, 1, aperm.p, nnzM, P->ar_val, s);
+    }
+    if (combo == 7) {
+      P->dvec.alloc(n > 0 ? n : 1);
+      dscal_vector(P->lc_ptr.p, P->lc_val.p, n, P->dvec.p, s);
+    }
+    if (combo == 5 || combo == 7) {
+      P->nnzF = nnzL;
+      P->fac.alloc(nnzL > 0 ? nnzL : 1);
+      P->work.alloc(nnzL > 0 ? nnzL : 1);
+    }
+  } else if (combo == 6) {
+    // to_csr(M) (kernels.hpp:475-478) + find_diag_positions
+    P->ar_ptr.alloc((int64_t)n + 1);
+    P->ar_idx.alloc(nnzM > 0 ? nnzM : 1);
+    DBuf<int32_t> aperm(nnzM > 0 ? nnzM : 1);
+    transpose(P->m_ptr.p, P->m_idx.p, n, n, nnzM, P->ar_ptr.p, P->ar_idx.p, aperm.p, s);
+    values_from(mval, nnzM, 1, aperm.p, nnzM, P->ar_val, s);
+    P->diag.alloc(n > 0 ? n : 1);
+    find_diag_positions(P->ar_ptr.p, P->ar_idx.p, n, P->diag.p, s);
+    P->nnzF = nnzM;
+    P->fac.alloc(nnzM > 0 ? nnzM : 1);
+    P->work.alloc(nnzM > 0 ? nnzM : 1);
+  }
+
+  // vectors
+  const int64_t nv = (int64_t)n * S;
+  if (combo != 7) {
+    std::vector<double> hv;
+    const double* src_h = vin_h;
+    if (!vin_h) {
+      hv.resize((size_t)nv);
+      for (int32_t sys = 0; sys < S; ++sys)
+        sfg_gen_vector(n, seed + (uint64_t)sys, hv.data() + (size_t)sys * n);
+      src_h = hv.data();
+    }
+    P->staging.alloc(nv > 0 ? 2 * nv : 1);
+    P->vin.alloc(nv > 0 ? nv : 1);
+    if (nv > 0) {
+      SFG_CUDA(cudaMemcpyAsync(P->staging.p, src_h, sizeof(double) * (size_t)nv,
+                               cudaMemcpyHostToDevice, s));
+      interleave(P->staging.p, n, S, P->vin.p, s);
+    }
+    P->vout.alloc(nv > 0 ? nv : 1);
+    if (combo == 1 || combo == 4 || combo == 8)
+      P->vmid.alloc(nv > 0 ? nv : 1);
+  }
+  P->counter.alloc(1);
+  P->err.alloc(1);
+  SFG_CUDA(cudaStreamSynchronize(s));
+}
+
+ExecArgs exec_args(sfg_plan* P) {
+  ExecArgs a;
+  a.n = P->n;
+  a.nsys = P->nsys;
+  a.order = P->order.p;
+  a.counter = P->counter.p;
+  a.err = P->err.p;
+  a.lr_ptr = P->lr_ptr.p;
+  a.lr_idx = P->lr_idx.p;
+  a.lr_val = P->lr_val.p;
+  a.lt_ptr = P->lt_ptr.p;
+  a.lt_idx = P->lt_idx.p;
+  a.lt_val = P->lt_val.p;
+  a.ar_ptr = P->ar_ptr.p;
+  a.ar_idx = P->ar_idx.p;
+  a.ar_val = P->ar_val.p;
+  a.diag = P->diag.p;
+  a.lc_ptr = P->lc_ptr.p;
+  a.lc_idx = P->lc_idx.p;
+  a.lc_val = P->lc_val.p;
+  a.rv_ptr = P->rv_ptr.p;
+  a.rv_col = P->rv_col.p;
+  a.rv_pos = P->rv_pos.p;
+  a.dvec = P->dvec.p;
+  a.vin = P->vin.p;
+  a.vmid = P->vmid.p;
+  a.vout = P->vout.p;
+  a.fac = P->fac.p;
+  a.work = P->work.p;
+  return a;
+}
+
+void ensure_events(sfg_plan* P) {
+  for (auto& e : P->ev)
+    if (!e)
+      SFG_CUDA(cudaEventCreate(&e));
+}
+
+// The main executor launch for a ticket range and phase mask.
+void launch_main(sfg_plan* P, const ExecArgs& a) {
+  switch (P->combo) {
+  case 1:
+  case 4:
+  case 8:
+    launch_trsv_pair(P->combo, a, P->stream);
+    break;
+  case 5:
+  case 7:
+    launch_ic0(P->combo, a, P->stream);
+    break;
+  case 6:
+    launch_ilu0(a, P->stream);
+    break;
+  }
+}
+
+void do_inspect(sfg_plan* P) {
+  cudaStream_t s = P->stream;
+  const int32_t n = P->n;
+  const int combo = P->combo;
+  const bool two_segments = combo == 4 || combo == 8;
+  P->ntickets = two_segments ? 2 * (int64_t)n : n;
+  P->order.alloc(P->ntickets > 0 ? P->ntickets : 1);
+  DBuf<int32_t> level(n > 0 ? n : 1);
+  const int32_t *ptr = nullptr, *idx = nullptr;
+  switch (combo) {
+  case 1:
+  case 4:
+  case 8:
+    ptr = P->lr_ptr.p;
+    idx = P->lr_idx.p;
+    break;
+  case 5:
+  case 7:
+    ptr = P->rv_ptr.p;
+    idx = P->rv_col.p;
+    break;
+  case 6:
+    ptr = P->ar_ptr.p;
+    idx = P->ar_idx.p;
+    break;
+  }
+  const int32_t P1 = levels_syncfree(ptr, idx, n, +1, level.p, s);
+  std::vector<int64_t> w1;
+  order_by_level(level.p, n, P1, P->order.p, &w1, s);
+  P->wave_ptr = w1;
+  P->seg2_start_wave = -1;
+  if (combo == 4) {
+    iota_i32_kernel<<<grid_for(n), 256, 0, s>>>(P->order.p + n, n, 0);
+    count_launch();
+    P->seg2_start_wave = (int32_t)P->wave_ptr.size() - 1;
+    P->wave_ptr.push_back(2 * (int64_t)n);
+  } else if (combo == 8) {
+    const int32_t P2 = levels_syncfree(P->lt_ptr.p, P->lt_idx.p, n, -1, level.p, s);
+    std::vector<int64_t> w2;
+    order_by_level(level.p, n, P2, P->order.p + n, &w2, s);
+    P->seg2_start_wave = (int32_t)P->wave_ptr.size() - 1;
+    for (size_t k = 1; k < w2.size(); ++k)
+      P->wave_ptr.push_back(w2[k] + n);
+  }
+  SFG_CUDA(cudaStreamSynchronize(s));
+  P->inspected = true;
+}
+
+// ---- parity DAGs ---------------------------------------------------------
+void build_cost(sfg_plan* P, int kind, const int32_t* ptr, const int32_t* idx,
+                const int32_t* ptr2, const int32_t* aux1, const int32_t* aux2, DevDag& g) {
+  g.cost.alloc(P->n > 0 ? P->n : 1);
+  if (P->n > 0) {
+    cost_kernel<<<grid_for(P->n), 256, 0, P->stream>>>(kind, P->n, ptr, idx, ptr2, aux1, aux2,
+                                                       g.cost.p);
+    count_launch();
+  }
+}
+
+void dag_from_structure(sfg_plan* P, const int32_t* ptr, const int32_t* idx, int64_t nent,
+                        int mode, DevDag& g) {
+  DBuf<uint64_t> keys(nent > 0 ? nent : 1);
+  if (nent > 0) {
+    edge_keys_kernel<<<grid_for((int64_t)P->n * 32), 256, 0, P->stream>>>(
+        ptr, idx, P->n, mode, P->n, 0, 0, keys.p);
+    count_launch();
+  }
+  csr_from_edge_keys(keys, nent, P->n, g, P->stream);
+}
+
+void edgeless(sfg_plan* P, DevDag& g) {
+  g.nvert = P->n;
+  g.nedges = 0;
+  g.ptr.alloc((int64_t)P->n + 1);
+  SFG_CUDA(cudaMemsetAsync(g.ptr.p, 0, sizeof(int32_t) * ((size_t)P->n + 1), P->stream));
+  g.idx.alloc(1);
+}
+
+void build_g(sfg_plan* P, int which) {
+  auto g = std::make_unique<DevDag>();
+  const int c = P->combo;
+  const int32_t n = P->n;
+  cudaStream_t s = P->stream;
+  if (which == 1) { // build_g1 (dag.hpp:319-337)
+    if (c == 1 || c == 4 || c == 8) {
+      dag_from_structure(P, P->lr_ptr.p, P->lr_idx.p, P->nnzL, EM_ROWS_LOWER, *g);
+      build_cost(P, CK_ROWNNZ, P->lr_ptr.p, nullptr, nullptr, nullptr, nullptr, *g);
+    } else if (c == 5) {
+      dag_from_structure(P, P->lc_ptr.p, P->lc_idx.p, P->nnzL, EM_COLS_BELOW, *g);
+      build_cost(P, CK_IC0, P->lc_ptr.p, nullptr, P->rv_ptr.p, P->rv_col.p, P->rv_pos.p, *g);
+    } else if (c == 6) {
+      dag_from_structure(P, P->ar_ptr.p, P->ar_idx.p, P->nnzM, EM_ROWS_LOWER, *g);
+      build_cost(P, CK_ILU0, P->ar_ptr.p, P->ar_idx.p, nullptr, P->diag.p, nullptr, *g);
+    } else if (c == 7) {
+      edgeless(P, *g);
+      build_cost(P, CK_ROWNNZ, P->lc_ptr.p, nullptr, nullptr, nullptr, nullptr, *g);
+    }
+  } else { // build_g2 (dag.hpp:339-370)
+    if (c == 1) {
+      dag_from_structure(P, P->lr_ptr.p, P->lr_idx.p, P->nnzL, EM_ROWS_LOWER, *g);
+      build_cost(P, CK_ROWNNZ, P->lr_ptr.p, nullptr, nullptr, nullptr, nullptr, *g);
+    } else if (c == 4) {
+      edgeless(P, *g);
+      build_cost(P, CK_ROWNNZ, P->m_ptr.p, nullptr, nullptr, nullptr, nullptr, *g);
+    } else if (c == 5) {
+      dag_from_structure(P, P->lc_ptr.p, P->lc_idx.p, P->nnzL, EM_COLS_BELOW, *g);
+      build_cost(P, CK_TRSV_CSC, nullptr, nullptr, P->rv_ptr.p, nullptr, nullptr, *g);
+    } else if (c == 6) {
+      dag_from_structure(P, P->ar_ptr.p, P->ar_idx.p, P->nnzM, EM_ROWS_LOWER, *g);
+      build_cost(P, CK_UNIT, P->ar_ptr.p, P->ar_idx.p, nullptr, nullptr, nullptr, *g);
+    } else if (c == 7) {
+      dag_from_structure(P, P->lc_ptr.p, P->lc_idx.p, P->nnzL, EM_COLS_BELOW, *g);
+      build_cost(P, CK_IC0, P->lc_ptr.p, nullptr, P->rv_ptr.p, P->rv_col.p, P->rv_pos.p, *g);
+    } else if (c == 8) {
+      dag_from_structure(P, P->lt_ptr.p, P->lt_idx.p, P->nnzL, EM_LT_REV, *g);
+      build_cost(P, CK_LT_REV, P->lt_ptr.p, nullptr, nullptr, nullptr, nullptr, *g);
+    }
+  }
+  (void)n;
+  SFG_CUDA(cudaStreamSynchronize(s));
+  P->dags[which - 1] = std::move(g);
+}
+
+void build_fdep(sfg_plan* P) {
+  cudaStream_t s = P->stream;
+  const int32_t n = P->n;
+  auto f = std::make_unique<DevDag>();
+  f->nvert = n;
+  f->ptr.alloc((int64_t)n + 1);
+  DBuf<int32_t> cnt((int64_t)n + 1);
+  fdep_count_kernel<<<grid_for((int64_t)n + 1), 256, 0, s>>>(P->combo, n, P->m_ptr.p,
+                                                              P->rv_ptr.p, cnt.p);
+  count_launch();
+  size_t bytes = 0;
+  SFG_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, bytes, cnt.p, f->ptr.p, n + 1, s));
+  DBuf<char> tmp((int64_t)bytes);
+  SFG_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, bytes, cnt.p, f->ptr.p, n + 1, s));
+  int32_t nnz = 0;
+  SFG_CUDA(cudaMemcpyAsync(&nnz, f->ptr.p + n, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+  SFG_CUDA(cudaStreamSynchronize(s));
+  f->nedges = nnz;
+  f->idx.alloc(nnz > 0 ? nnz : 1);
+  fdep_fill_kernel<<<grid_for(n), 256, 0, s>>>(P->combo, n, P->m_ptr.p, P->rv_ptr.p,
+                                               P->rv_col.p, f->ptr.p, f->idx.p);
+  count_launch();
+  SFG_CUDA(cudaStreamSynchronize(s));
+  P->fdep = std::move(f);
+}
+
+__global__ void cost_concat_kernel(const int64_t* a, const int64_t* b, int32_t n, int64_t* out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < 2 * (int64_t)n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = i < n ? a[i] : b[i - n];
+}
+
+void build_joint(sfg_plan* P) {
+  if (!P->dags[0])
+    build_g(P, 1);
+  if (!P->dags[1])
+    build_g(P, 2);
+  if (!P->fdep)
+    build_fdep(P);
+  const DevDag& g1 = *P->dags[0];
+  const DevDag& g2 = *P->dags[1];
+  const DevDag& f = *P->fdep;
+  cudaStream_t s = P->stream;
+  const int32_t n = P->n;
+  const int64_t ne = g1.nedges + g2.nedges + f.nedges;
+  DBuf<uint64_t> keys(ne > 0 ? ne : 1);
+  // joint_dag (dag.hpp:222-238): E1, E2 offset by |V1|, (j, |V1| + i) per F_ij
+  if (g1.nedges)
+    edge_keys_kernel<<<grid_for((int64_t)n * 32), 256, 0, s>>>(g1.ptr.p, g1.idx.p, n, EM_SUCC,
+                                                               n, 0, 0, keys.p);
+  if (g2.nedges)
+    edge_keys_kernel<<<grid_for((int64_t)n * 32), 256, 0, s>>>(g2.ptr.p, g2.idx.p, n, EM_SUCC,
+                                                               n, n, n, keys.p + g1.nedges);
+  if (f.nedges)
+    edge_keys_kernel<<<grid_for((int64_t)n * 32), 256, 0, s>>>(
+        f.ptr.p, f.idx.p, n, EM_FDEP, n, 0, n, keys.p + g1.nedges + g2.nedges);
+  count_launch(3);
+  auto j = std::make_unique<DevDag>();
+  csr_from_edge_keys(keys, ne, 2 * n, *j, s);
+  j->cost.alloc(2 * (int64_t)n > 0 ? 2 * (int64_t)n : 1);
+  cost_concat_kernel<<<grid_for(2 * (int64_t)n), 256, 0, s>>>(g1.cost.p, g2.cost.p, n, j->cost.p);
+  count_launch();
+  SFG_CUDA(cudaStreamSynchronize(s));
+  P->dags[2] = std::move(j);
+}
+
+void ensure_dag(sfg_plan* P, int which) {
+  if (which == 3) {
+    if (!P->dags[2])
+      build_joint(P);
+  } else if (!P->dags[which - 1]) {
+    build_g(P, which);
+  }
+}
+
+void ensure_levels(sfg_plan* P, int which) {
+  if (P->have_levels[which - 1])
+    return;
+  ensure_dag(P, which);
+  const DevDag& g = *P->dags[which - 1];
+  if (!edges_ascend(g, P->stream))
+    throw InvalidArgument("dependence cycle: edge does not ascend");
+  DevDag pred;
+  flip_dag(g, pred, P->stream);
+  const int32_t nv = g.nvert;
+  P->lev[which - 1].alloc(nv > 0 ? nv : 1);
+  P->hgt[which - 1].alloc(nv > 0 ? nv : 1);
+  P->slk[which - 1].alloc(nv > 0 ? nv : 1);
+  const int32_t Pc = levels_syncfree(pred.ptr.p, pred.idx.p, nv, +1, P->lev[which - 1].p,
+                                     P->stream);
+  heights_syncfree(g.ptr.p, g.idx.p, nv, P->hgt[which - 1].p, P->stream);
+  slack_from(P->lev[which - 1].p, P->hgt[which - 1].p, Pc, nv, P->slk[which - 1].p, P->stream);
+  SFG_CUDA(cudaStreamSynchronize(P->stream));
+  P->crit[which - 1] = Pc;
+  P->have_levels[which - 1] = true;
+}
+
+// ---- error word ------------------------------------------------------------
+int ferr_kind_of(int combo, int kernel) {
+  switch (combo) {
+  case 5:
+    return kernel == 1 ? SFG_FERR_NONPOS_PIVOT : SFG_FERR_ZERO_DIAG_SOLVE;
+  case 6:
+    return SFG_FERR_ZERO_PIVOT;
+  case 7:
+    return SFG_FERR_NONPOS_PIVOT;
+  default:
+    return SFG_FERR_ZERO_DIAG_SOLVE;
+  }
+}
+
+const char* ferr_text(int kind) {
+  switch (kind) {
+  case SFG_FERR_ZERO_DIAG_SOLVE:
+    return "zero diagonal in triangular solve";
+  case SFG_FERR_NONPOS_PIVOT:
+    return "non-positive pivot";
+  case SFG_FERR_ZERO_PIVOT:
+    return "zero pivot";
+  case SFG_FERR_ZERO_DIAG_SCALE:
+    return "zero diagonal";
+  default:
+    return "invalid matrix";
+  }
+}
+
+sfg_status check_error_word(sfg_plan* P) {
+  unsigned long long key = ~0ull;
+  SFG_CUDA(cudaMemcpyAsync(&key, P->err.p, sizeof(key), cudaMemcpyDeviceToHost, P->stream));
+  SFG_CUDA(cudaStreamSynchronize(P->stream));
+  if (key == ~0ull)
+    return SFG_OK;
+  const int kernel = (int)(key >> 62) + 1;
+  const int32_t index = (int32_t)(key & 0x7fffffffull);
+  const int kind = ferr_kind_of(P->combo, kernel);
+  return set_err(P, SFG_ERR_FACTORIZATION,
+                 std::string(ferr_text(kind)) + " at index " + std::to_string(index), kind,
+                 index);
+}
+
+} // namespace
+
+// ===========================================================================
+extern "C" {
+
+const char* sfg_version(void) { return "sfgpu 0.1 (sm_100a)"; }
+
+sfg_status sfg_device_check(int32_t* device_count, int32_t* sms) {
+  int cnt = 0;
+  if (cudaGetDeviceCount(&cnt) != cudaSuccess || cnt <= 0) {
+    cudaGetLastError();
+    if (device_count)
+      *device_count = 0;
+    return SFG_ERR_NO_DEVICE;
+  }
+  if (device_count)
+    *device_count = cnt;
+  if (sms) {
+    int dev = 0, v = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    *sms = v;
+  }
+  return SFG_OK;
+}
+
+sfg_status sfg_plan_create(int32_t combo, int32_t n, const int32_t* colptr,
+                           const int32_t* rowidx, const double* values, int32_t nsys,
+                           const double* vin, uint64_t seed, sfg_plan** out) {
+  if (!out)
+    return SFG_ERR_INVALID_ARGUMENT;
+  *out = nullptr;
+  if (!(combo == 1 || combo == 4 || combo == 5 || combo == 6 || combo == 7 || combo == 8))
+    return SFG_ERR_INVALID_ARGUMENT;
+  if (n < 0 || !colptr || (colptr[n] > 0 && (!rowidx || !values)))
+    return SFG_ERR_INVALID_ARGUMENT;
+  if (nsys < 1 || !pow2_upto32(nsys) || (nsys > 1 && combo != 1 && combo != 8))
+    return SFG_ERR_INVALID_ARGUMENT;
+  int cnt = 0;
+  if (cudaGetDeviceCount(&cnt) != cudaSuccess || cnt <= 0) {
+    cudaGetLastError();
+    return SFG_ERR_NO_DEVICE;
+  }
+  auto* P = new sfg_plan();
+  P->combo = combo;
+  P->n = n;
+  P->nsys = nsys;
+  cudaGetDevice(&P->device);
+  const sfg_status st = guarded(P, [&] {
+    validate_csc(n, colptr, rowidx);
+    LaunchScope ls(P);
+    SFG_CUDA(cudaStreamCreateWithFlags(&P->own_stream, cudaStreamNonBlocking));
+    P->stream = P->own_stream;
+    build_plan(P, colptr, rowidx, values, vin, seed);
+    ensure_events(P);
+    return SFG_OK;
+  });
+  if (st != SFG_OK) {
+    // keep the plan alive only to report; callers destroy it on error
+    *out = P;
+    return st;
+  }
+  *out = P;
+  return SFG_OK;
+}
+
+sfg_status sfg_plan_destroy(sfg_plan* P) {
+  if (!P)
+    return SFG_OK;
+  {
+    DeviceScope ds(P->device);
+    if (P->stream)
+      cudaStreamSynchronize(P->stream);
+    for (auto& e : P->ev)
+      if (e)
+        cudaEventDestroy(e);
+    if (P->own_stream)
+      cudaStreamDestroy(P->own_stream);
+  }
+  delete P;
+  return SFG_OK;
+}
+
+sfg_status sfg_plan_set_stream(sfg_plan* P, void* stream) {
+  if (!P)
+    return SFG_ERR_INVALID_ARGUMENT;
+  P->stream = stream ? (cudaStream_t)stream : P->own_stream;
+  return SFG_OK;
+}
+
+sfg_status sfg_plan_info(const sfg_plan* P, int32_t* combo, int32_t* n, int32_t* nsys,
+                         int64_t* nnz_factor, int64_t* out_len) {
+  if (!P)
+    return SFG_ERR_INVALID_ARGUMENT;
+  if (combo)
+    *combo = P->combo;
+  if (n)
+    *n = P->n;
+  if (nsys)
+    *nsys = P->nsys;
+  if (nnz_factor)
+    *nnz_factor = P->nnzF;
+  if (out_len) {
+    const int c = P->combo;
+    *out_len = (c == 1 || c == 4 || c == 8) ? 2 * (int64_t)P->n : P->nnzF + P->n;
+  }
+  return SFG_OK;
+}
+
+sfg_status sfg_set_vin(sfg_plan* P, const double* vin_host) {
+  if (!P || !vin_host || P->combo == 7)
+    return SFG_ERR_INVALID_ARGUMENT;
+  return guarded(P, [&] {
+    DeviceScope ds(P->device);
+    LaunchScope ls(P);
+    const int64_t nv = (int64_t)P->n * P->nsys;
+    if (nv == 0)
+      return SFG_OK;
+    if (P->nsys == 1) {
+      SFG_CUDA(cudaMemcpyAsync(P->vin.p, vin_host, sizeof(double) * (size_t)nv,
+                               cudaMemcpyHostToDevice, P->stream));
+    } else {
+      SFG_CUDA(cudaMemcpyAsync(P->staging.p, vin_host, sizeof(double) * (size_t)nv,
+                               cudaMemcpyHostToDevice, P->stream));
+      interleave(P->staging.p, P->n, P->nsys, P->vin.p, P->stream);
+    }
+    return SFG_OK;
+  });
+}
+
+sfg_status sfg_inspect(sfg_plan* P) {
+  if (!P)
+    return SFG_ERR_INVALID_ARGUMENT;
+  return guarded(P, [&] {
+    DeviceScope ds(P->device);
+    LaunchScope ls(P);
+    do_inspect(P);
+    return SFG_OK;
+  });
+}
+
+sfg_status sfg_get_dag(sfg_plan* P, int32_t which, int32_t* nvert, int64_t* nedges,
+                       int32_t* succptr, int32_t* succ, int64_t* cost) {
+  if (!P || which < 1 || which > 3)
+    return SFG_ERR_INVALID_ARGUMENT;
+  return guarded(P, [&] {
+    DeviceScope ds(P->device);
+    LaunchScope ls(P);
+    ensure_dag(P, which);
+    const DevDag& g = *P->dags[which - 1];
+    if (nvert)
+      *nvert = g.nvert;
+    if (nedges)
+      *nedges = g.nedges;
+    if (succptr)
+      SFG_CUDA(cudaMemcpy(succptr, g.ptr.p, sizeof(int32_t) * ((size_t)g.nvert + 1),
+                          cudaMemcpyDeviceToHost));
+    if (succ && g.nedges)
+      SFG_CUDA(cudaMemcpy(succ, g.idx.p, sizeof(int32_t) * (size_t)g.nedges,
+                          cudaMemcpyDeviceToHost));
+    if (cost && g.nvert)
+      SFG_CUDA(cudaMemcpy(cost, g.cost.p, sizeof(int64_t) * (size_t)g.nvert,
+                          cudaMemcpyDeviceToHost));
+    return SFG_OK;
+  });
+}
+
+sfg_status sfg_get_interdep(sfg_plan* P, int32_t* nrows, int32_t* ncols, int64_t* nnz,
+                            int32_t* rowptr, int32_t* colidx) {
+  if (!P)
+    return SFG_ERR_INVALID_ARGUMENT;
+  return guarded(P, [&] {
+    DeviceScope ds(P->device);
+    LaunchScope ls(P);
+    if (!P->fdep)
+      build_fdep(P);
+    const DevDag& f = *P->fdep;
+    if (nrows)
+      *nrows = P->n;
+    if (ncols)
+      *ncols = P->n;
+    if (nnz)
+      *nnz = f.nedges;
+    if (rowptr)
+      SFG_CUDA(cudaMemcpy(rowptr, f.ptr.p, sizeof(int32_t) * ((size_t)P->n + 1),
+                          cudaMemcpyDeviceToHost));
+    if (colidx && f.nedges)
+      SFG_CUDA(cudaMemcpy(colidx, f.idx.p, sizeof(int32_t) * (size_t)f.nedges,
+                          cudaMemcpyDeviceToHost));
+    return SFG_OK;
+  });
+}
+
+sfg_status sfg_get_levels(sfg_plan* P, int32_t which, int32_t* level, int32_t* height,
+                          int32_t* slack, int32_t* critical_path) {
+  if (!P || which < 1 || which > 3)
+    return SFG_ERR_INVALID_ARGUMENT;
+  return guarded(P, [&] {
+    DeviceScope ds(P->device);
+    LaunchScope ls(P);
+    ensure_levels(P, which);
+    const int32_t nv = P->dags[which - 1]->nvert;
+    if (level && nv)
+      SFG_CUDA(cudaMemcpy(level, P->lev[which - 1].p, sizeof(int32_t) * (size_t)nv,
+                          cudaMemcpyDeviceToHost));
+    if (height && nv)
+      SFG_CUDA(cudaMemcpy(height, P->hgt[which - 1].p, sizeof(int32_t) * (size_t)nv,
+                          cudaMemcpyDeviceToHost));
+    if (slack && nv)
+      SFG_CUDA(cudaMemcpy(slack, P->slk[which - 1].p, sizeof(int32_t) * (size_t)nv,
+                          cudaMemcpyDeviceToHost));
+    if (critical_path)
+      *critical_path = P->crit[which - 1];
+    return SFG_OK;
+  });
+}
+
+sfg_status sfg_compute_reuse(sfg_plan* P, double* reuse) {
+  if (!P || !reuse)
+    return SFG_ERR_INVALID_ARGUMENT;
+  // dag.hpp:374-431 from the nonzero counts
+  const double dn = (double)P->n;
+  const double L = (double)P->lower_count;
+  const double A = (double)P->nnzM;
+  switch (P->combo) {
+  case 1:
+  case 8:
+    *reuse = (2 * dn + 2 * L) / std::max(2 * dn + L, L + 2 * dn);
+    break;
+  case 4:
+    *reuse = 2 * dn / std::max(2 * dn + L, A + 2 * dn);
+    break;
+  case 5:
+  case 7:
+    *reuse = 2 * L / std::max(L, L + 2 * dn);
+    break;
+  case 6:
+    *reuse = 2 * A / std::max(A, L + 2 * dn);
+    break;
+  default:
+    return SFG_ERR_INVALID_ARGUMENT;
+  }
+  return SFG_OK;
+}
+
+sfg_status sfg_get_schedule(sfg_plan* P, int64_t* nentries, uint8_t* tags, int32_t* iters,
+                            int32_t* nwaves, int64_t* wave_ptr) {
+  if (!P)
+    return SFG_ERR_INVALID_ARGUMENT;
+  if (!P->inspected)
+    return set_err(P, SFG_ERR_LOGIC, "sfg_inspect has not run");
+  return guarded(P, [&] {
+    DeviceScope ds(P->device);
+    const bool fused_task = !(P->combo == 4 || P->combo == 8);
+    const int64_t ne = fused_task ? 2 * P->ntickets : P->ntickets;
+    if (nentries)
+      *nentries = ne;
+    if (nwaves)
+      *nwaves = (int32_t)P->wave_ptr.size() - 1;
+    if (wave_ptr) {
+      for (size_t k = 0; k < P->wave_ptr.size(); ++k)
+        wave_ptr[k] = fused_task ? 2 * P->wave_ptr[k] : P->wave_ptr[k];
+    }
+    if (tags || iters) {
+      std::vector<int32_t> ord((size_t)P->ntickets);
+      if (P->ntickets)
+        SFG_CUDA(cudaMemcpy(ord.data(), P->order.p, sizeof(int32_t) * ord.size(),
+                            cudaMemcpyDeviceToHost));
+      for (int64_t t = 0; t < P->ntickets; ++t) {
+        if (fused_task) {
+          if (tags) {
+            tags[2 * t] = 1;
+            tags[2 * t + 1] = 2;
+          }
+          if (iters) {
+            iters[2 * t] = ord[(size_t)t];
+            iters[2 * t + 1] = ord[(size_t)t];
+          }
+        } else {
+          if (tags)
+            tags[t] = t < P->n ? 1 : 2;
+          if (iters)
+            iters[t] = (P->combo == 8 && t >= P->n) ? P->n - 1 - ord[(size_t)t]
+                                                    : ord[(size_t)t];
+        }
+      }
+    }
+    return SFG_OK;
+  });
+}
+
+sfg_status sfg_execute_fused(sfg_plan* P) {
+  if (!P)
+    return SFG_ERR_INVALID_ARGUMENT;
+  if (!P->inspected)
+    return set_err(P, SFG_ERR_LOGIC, "sfg_inspect has not run");
+  return guarded(P, [&] {
+    DeviceScope ds(P->device);
+    LaunchScope ls(P);
+    const int64_t nv = (int64_t)P->n * P->nsys;
+    FillRegion r[3];
+    int nr = 0;
+    switch (P->combo) {
+    case 1:
+    case 8:
+      r[nr++] = {P->vmid.p, nv};
+      r[nr++] = {P->vout.p, nv};
+      break;
+    case 4:
+      r[nr++] = {P->vmid.p, nv};
+      break;
+    case 5:
+    case 6:
+      r[nr++] = {P->fac.p, P->nnzF};
+      r[nr++] = {P->vout.p, nv};
+      break;
+    case 7:
+      r[nr++] = {P->fac.p, P->nnzF};
+      break;
+    }
+    SFG_CUDA(cudaEventRecord(P->ev[0], P->stream));
+    launch_prep(r, nr, P->counter.p, P->err.p, P->stream);
+    SFG_CUDA(cudaEventRecord(P->ev[1], P->stream));
+    ExecArgs a = exec_args(P);
+    a.phase = 3;
+    a.t_begin = 0;
+    a.t_end = P->ntickets;
+    launch_main(P, a);
+    SFG_CUDA(cudaEventRecord(P->ev[2], P->stream));
+    SFG_CUDA(cudaEventRecord(P->ev[3], P->stream));
+    P->timed = true;
+    return SFG_OK;
+  });
+}
+
+sfg_status sfg_execute_unfused(sfg_plan* P) {
+  if (!P)
+    return SFG_ERR_INVALID_ARGUMENT;
+  if (!P->inspected)
+    return set_err(P, SFG_ERR_LOGIC, "sfg_inspect has not run");
+  return guarded(P, [&] {
+    DeviceScope ds(P->device);
+    LaunchScope ls(P);
+    const int64_t nv = (int64_t)P->n * P->nsys;
+    const int c = P->combo;
+    const int32_t n = P->n;
+    ExecArgs a = exec_args(P);
+    SFG_CUDA(cudaEventRecord(P->ev[0], P->stream));
+    // ---- kernel 1
+    FillRegion r1[2];
+    int n1 = 0;
+    if (c == 1 || c == 4 || c == 8)
+      r1[n1++] = {P->vmid.p, nv};
+    else if (c == 5 || c == 6)
+      r1[n1++] = {P->fac.p, P->nnzF};
+    launch_prep(r1, n1, P->counter.p, P->err.p, P->stream);
+    SFG_CUDA(cudaEventRecord(P->ev[1], P->stream));
+    a.phase = 1;
+    a.t_begin = 0;
+    a.t_end = n;
+    if (c == 7)
+      launch_dscal(a, P->stream);
+    else
+      launch_main(P, a);
+    // ---- kernel 2 (stream order is the barrier between the kernels)
+    FillRegion r2[2];
+    int n2 = 0;
+    if (c == 1 || c == 8 || c == 5 || c == 6)
+      r2[n2++] = {P->vout.p, nv};
+    else if (c == 7)
+      r2[n2++] = {P->fac.p, P->nnzF};
+    launch_prep(r2, n2, P->counter.p, nullptr, P->stream);
+    a.phase = 2;
+    if (c == 4 || c == 8) {
+      a.t_begin = n;
+      a.t_end = 2 * (int64_t)n;
+    }
+    launch_main(P, a);
+    SFG_CUDA(cudaEventRecord(P->ev[2], P->stream));
+    SFG_CUDA(cudaEventRecord(P->ev[3], P->stream));
+    P->timed = true;
+    return SFG_OK;
+  });
+}
+
+sfg_status sfg_synchronize(sfg_plan* P) {
+  if (!P)
+    return SFG_ERR_INVALID_ARGUMENT;
+  return guarded(P, [&] {
+    DeviceScope ds(P->device);
+    SFG_CUDA(cudaStreamSynchronize(P->stream));
+    return check_error_word(P);
+  });
+}
+
+sfg_status sfg_collect_outputs(sfg_plan* P, double* out, int64_t cap) {
+  if (!P || (!out && cap > 0))
+    return SFG_ERR_INVALID_ARGUMENT;
+  return guarded(P, [&] {
+    DeviceScope ds(P->device);
+    LaunchScope ls(P);
+    const sfg_status e = check_error_word(P);
+    if (e != SFG_OK)
+      return e;
+    const int c = P->combo;
+    const int32_t n = P->n, S = P->nsys;
+    cudaStream_t s = P->stream;
+    if (c == 1 || c == 4 || c == 8) {
+      const int64_t need = 2 * (int64_t)n * S;
+      if (cap < need)
+        throw InvalidArgument("output buffer too small");
+      if (n == 0)
+        return SFG_OK;
+      if (S == 1) {
+        SFG_CUDA(cudaMemcpyAsync(out, P->vmid.p, sizeof(double) * (size_t)n,
+                                 cudaMemcpyDeviceToHost, s));
+        SFG_CUDA(cudaMemcpyAsync(out + n, P->vout.p, sizeof(double) * (size_t)n,
+                                 cudaMemcpyDeviceToHost, s));
+      } else {
+        collect_pair_kernel<<<grid_for((int64_t)n * S), 256, 0, s>>>(P->vmid.p, P->vout.p, n, S,
+                                                                     P->staging.p);
+        count_launch();
+        SFG_CUDA(cudaMemcpyAsync(out, P->staging.p, sizeof(double) * (size_t)need,
+                                 cudaMemcpyDeviceToHost, s));
+      }
+    } else {
+      const int64_t need = P->nnzF + n;
+      if (cap < need)
+        throw InvalidArgument("output buffer too small");
+      if (P->nnzF)
+        SFG_CUDA(cudaMemcpyAsync(out, P->fac.p, sizeof(double) * (size_t)P->nnzF,
+                                 cudaMemcpyDeviceToHost, s));
+      const double* tail = c == 7 ? P->dvec.p : P->vout.p;
+      if (n)
+        SFG_CUDA(cudaMemcpyAsync(out + P->nnzF, tail, sizeof(double) * (size_t)n,
+                                 cudaMemcpyDeviceToHost, s));
+    }
+    SFG_CUDA(cudaStreamSynchronize(s));
+    return SFG_OK;
+  });
+}
+
+sfg_status sfg_device_output(sfg_plan* P, int32_t which, void** dptr, int64_t* count) {
+  if (!P || !dptr)
+    return SFG_ERR_INVALID_ARGUMENT;
+  const int c = P->combo;
+  const int64_t nv = (int64_t)P->n * P->nsys;
+  if (c == 1 || c == 4 || c == 8) {
+    *dptr = which == 0 ? (void*)P->vmid.p : (void*)P->vout.p;
+    if (count)
+      *count = nv;
+  } else {
+    if (which == 0) {
+      *dptr = P->fac.p;
+      if (count)
+        *count = P->nnzF;
+    } else {
+      *dptr = c == 7 ? (void*)P->dvec.p : (void*)P->vout.p;
+      if (count)
+        *count = P->n;
+    }
+  }
+  return SFG_OK;
+}
+
+sfg_status sfg_last_error(const sfg_plan* P, int32_t* kind, int32_t* index, char* msg,
+                          int32_t msg_len) {
+  if (!P)
+    return SFG_ERR_INVALID_ARGUMENT;
+  if (kind)
+    *kind = P->ferr_kind;
+  if (index)
+    *index = P->ferr_index;
+  if (msg && msg_len > 0) {
+    const size_t k = std::min<size_t>(P->msg.size(), (size_t)msg_len - 1);
+    std::memcpy(msg, P->msg.data(), k);
+    msg[k] = 0;
+  }
+  return SFG_OK;
+}
+
+int64_t sfg_launch_count(const sfg_plan* P) { return P ? P->launches : -1; }
+
+sfg_status sfg_last_exec_ms(sfg_plan* P, float* total_ms, float* kernel_ms) {
+  if (!P || !P->timed)
+    return SFG_ERR_INVALID_ARGUMENT;
+  return guarded(P, [&] {
+    DeviceScope ds(P->device);
+    SFG_CUDA(cudaEventSynchronize(P->ev[3]));
+    if (total_ms)
+      SFG_CUDA(cudaEventElapsedTime(total_ms, P->ev[0], P->ev[3]));
+    if (kernel_ms)
+      SFG_CUDA(cudaEventElapsedTime(kernel_ms, P->ev[1], P->ev[2]));
+    return SFG_OK;
+  });
+}
+
+} // extern "C"

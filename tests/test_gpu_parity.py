@@ -1,0 +1,237 @@
+"""CUDA path (libsfgpu.so through the C-ABI) against the reference.
+
+* golden cases: outputs, DAGs, F, joint DAG, levels and reuse produced by the
+  unmodified reference (tests/golden) -- compared bit for bit;
+* BASELINE.json configurations at full size: compared with the oracle
+  (oracle/sf_oracle.c, itself pinned to the reference by test_oracle.py) on
+  the same seeded inputs -- bit for bit, and the north_star tolerance
+  (max relative error 1e-10) plus solve residuals as a second line;
+* error behaviour (FactorizationError index), idempotence, fused vs unfused,
+  and the schedule being a linear extension of the joint DAG.
+"""
+import numpy as np
+import pytest
+
+import paper_2111_12238_b200 as sf
+from conftest import GOLDEN_MATS, golden_matrix
+from oracle.oracle import Csc
+
+pytestmark = pytest.mark.gpu
+
+GPU_COMBOS = (1, 4, 5, 6, 7, 8)
+TOL = 1e-10  # north_star: fp64 values within max-relative-error 1e-10
+
+
+def as_sf(M) -> sf.CscMatrix:
+    return sf.CscMatrix(M.n, M.colptr, M.rowidx, M.values)
+
+
+def max_rel(got, want):
+    scale = max(1.0, float(np.max(np.abs(want)))) if want.size else 1.0
+    return float(np.max(np.abs(got - want))) / scale if want.size else 0.0
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _device():
+    from paper_2111_12238_b200 import abi
+    assert abi.device_available(), "B200 required: the -m gpu suite never skips"
+
+
+@pytest.mark.parametrize("name", GOLDEN_MATS)
+@pytest.mark.parametrize("combo", GPU_COMBOS)
+def test_golden_outputs_fused_and_unfused(golden, name, combo):
+    M = as_sf(golden_matrix(golden, name))
+    want = golden[f"{name}/c{combo}/outputs"]
+    st = sf.make_state(combo, M, seed=7)
+    sched = sf.make_fused_schedule(st)
+    sf.execute_fused(sched, st)
+    assert np.array_equal(sf.collect_outputs(st), want)
+    st.execute_unfused()
+    assert np.array_equal(st.collect_outputs(), want)
+    # idempotent re-execution (reset semantics, kernels.hpp:497-502)
+    st.execute_fused()
+    assert np.array_equal(st.collect_outputs(), want)
+
+
+@pytest.mark.parametrize("name", GOLDEN_MATS)
+@pytest.mark.parametrize("combo", (1, 4, 5, 6, 7))
+def test_golden_dags_levels(golden, name, combo):
+    M = as_sf(golden_matrix(golden, name))
+    key = f"{name}/c{combo}"
+    st = sf.make_state(combo, M)
+    for which in (1, 2):
+        g = st.dag(which)
+        assert np.array_equal(g.succptr, golden[f"{key}/g{which}_succptr"])
+        assert np.array_equal(g.succ, golden[f"{key}/g{which}_succ"])
+        assert np.array_equal(g.cost, golden[f"{key}/g{which}_cost"])
+        li = st.level_info(which)
+        assert np.array_equal(li.level, golden[f"{key}/g{which}_level"])
+        assert li.critical_path == golden[f"{key}/g{which}_P"][0]
+    f = sf.inter_dag(st)
+    assert np.array_equal(f.rowptr, golden[f"{key}/f_rowptr"])
+    assert np.array_equal(f.colidx, golden[f"{key}/f_colidx"])
+    j = sf.joint_dag(st)
+    assert np.array_equal(j.succptr, golden[f"{key}/j_succptr"])
+    assert np.array_equal(j.succ, golden[f"{key}/j_succ"])
+    assert np.array_equal(j.cost, golden[f"{key}/j_cost"])
+    lj = sf.level_info(st, 3)
+    assert np.array_equal(lj.level, golden[f"{key}/j_level"])
+    assert np.array_equal(lj.height, golden[f"{key}/j_height"])
+    assert np.array_equal(lj.slack, golden[f"{key}/j_slack"])
+    assert lj.critical_path == golden[f"{key}/j_P"][0]
+    assert sf.compute_reuse(st) == golden[f"{key}/reuse"][0]
+
+
+def _check_linear_extension(st, joint):
+    """Every joint-DAG edge u -> v is scheduled with u before v."""
+    sch = st.schedule()
+    n = st.n
+    pos = np.empty(2 * n, np.int64)
+    ids = np.where(sch.tags == 1, sch.iters, n + sch.iters)
+    assert np.array_equal(np.sort(ids), np.arange(2 * n))
+    pos[ids] = np.arange(len(ids))
+    src = np.repeat(np.arange(joint.nvert), np.diff(joint.succptr))
+    assert np.all(pos[src] < pos[joint.succ])
+    assert sch.wave_ptr[0] == 0 and sch.wave_ptr[-1] == len(ids)
+
+
+@pytest.mark.parametrize("name", GOLDEN_MATS)
+@pytest.mark.parametrize("combo", (1, 4, 5, 6, 7))
+def test_schedule_is_linear_extension(golden, name, combo):
+    M = as_sf(golden_matrix(golden, name))
+    st = sf.make_state(combo, M).inspect()
+    _check_linear_extension(st, st.dag(3))
+
+
+@pytest.mark.parametrize("name", GOLDEN_MATS)
+def test_combo8_structures_vs_oracle(orc, golden, name):
+    Mo = golden_matrix(golden, name)
+    st = sf.make_state(8, as_sf(Mo)).inspect()
+    for which in (1, 2):
+        g, w = st.dag(which), orc.build_g(8, which, Mo)
+        assert np.array_equal(g.succptr, w.succptr) and np.array_equal(g.succ, w.succ)
+        assert np.array_equal(g.cost, w.cost)
+    f, w = st.inter_dag(), orc.inter_dag(8, Mo)
+    assert np.array_equal(f.rowptr, w.rowptr) and np.array_equal(f.colidx, w.colidx)
+    j = st.dag(3)
+    wj = orc.joint_dag(orc.build_g(8, 1, Mo), orc.build_g(8, 2, Mo), w)
+    assert np.array_equal(j.succptr, wj.succptr) and np.array_equal(j.succ, wj.succ)
+    lj, wl = st.level_info(3), orc.level_info(wj)
+    assert np.array_equal(lj.level, wl.level) and np.array_equal(lj.height, wl.height)
+    _check_linear_extension(st, j)
+
+
+def test_breakdown_reports_reference_index(golden):
+    cp = golden["breakdown/colptr"]
+    M = sf.CscMatrix(len(cp) - 1, cp, golden["breakdown/rowidx"], golden["breakdown/values"])
+    st = sf.make_state(5, M, seed=1)
+    with pytest.raises(sf.FactorizationError) as e:
+        st.execute_fused()
+    assert e.value.index == golden["breakdown/c5_index"][0] == 7
+    assert "non-positive pivot" in str(e.value)
+    with pytest.raises(sf.FactorizationError):
+        st.execute_unfused()
+
+
+@pytest.mark.parametrize("combo", (1, 4, 8))
+def test_zero_diagonal_solve_error(orc, combo):
+    # a zero diagonal is rejected by lower_triangle (matrix.hpp:106-112)
+    M = sf.config_matrix(1, size=6)
+    vals = M.values.copy()
+    j = 9
+    p = M.colptr[j] + list(M.rowidx[M.colptr[j]:M.colptr[j + 1]]).index(j)
+    vals[p] = 0.0
+    with pytest.raises(sf.InvalidMatrixError, match="zero diagonal entry at column 9"):
+        sf.make_state(combo, sf.CscMatrix(M.n, M.colptr, M.rowidx, vals))
+
+
+def test_ilu0_zero_pivot_index(orc):
+    # row 3's pivot U_33 cancels to 0 -> "zero pivot" at the pivot row
+    D = np.array([[2.0, 1, 0, 0, 0], [1, 2, 0, 0, 0], [0, 0, 1, 1, 0], [0, 0, 1, 1, 1],
+                  [0, 0, 0, 1, 3]])
+    cp, ri, va = [0], [], []
+    for jj in range(5):
+        for ii in range(5):
+            if D[ii, jj] != 0:
+                ri.append(ii)
+                va.append(D[ii, jj])
+        cp.append(len(ri))
+    Mo = Csc(5, np.array(cp, np.int32), np.array(ri, np.int32), np.array(va))
+    from oracle.oracle import FactorizationError as OFE
+    with pytest.raises(OFE) as want:
+        orc.run_sequential(6, Mo, 7)
+    st = sf.make_state(6, as_sf(Mo))
+    with pytest.raises(sf.FactorizationError) as got:
+        st.execute_fused()
+    assert got.value.index == want.value.index == 3
+    assert "zero pivot" in str(got.value)
+
+
+def test_multisystem_golden(golden, orc):
+    # nsys systems with distinct values/vectors: each equals its own oracle run
+    for name in ("banded40", "grid10"):
+        Mo = golden_matrix(golden, name)
+        nsys = 4
+        rng = np.random.default_rng(3)
+        vals = np.concatenate([Mo.values * (1 + 0.01 * s) for s in range(nsys)])
+        vin = rng.uniform(-1, 1, nsys * Mo.n)
+        for combo in (1, 8):
+            st = sf.make_state(combo, as_sf(Mo), nsys=nsys, values=vals, vin=vin)
+            st.execute_fused()
+            got = st.collect_outputs().reshape(nsys, -1)
+            for s in range(nsys):
+                Ms = Csc(Mo.n, Mo.colptr, Mo.rowidx, vals[s * Mo.nnz:(s + 1) * Mo.nnz])
+                want = orc.run_sequential(combo, Ms, 7, vin=vin[s * Mo.n:(s + 1) * Mo.n])
+                assert np.array_equal(got[s], want)
+
+
+# ---- BASELINE.json configurations at full size --------------------------------
+CONFIG_COMBO = {1: 4, 2: 5, 3: 6, 4: 7}
+
+
+@pytest.mark.parametrize("cfg", (1, 2, 3, 4))
+def test_config_full_size_vs_oracle(orc, cfg):
+    M = sf.config_matrix(cfg)
+    combo = CONFIG_COMBO[cfg]
+    Mo = Csc(M.n, M.colptr, M.rowidx, M.values)
+    want = orc.run_sequential(combo, Mo, 7)
+    st = sf.make_state(combo, M, seed=7)
+    st.execute_fused()
+    got = st.collect_outputs()
+    assert max_rel(got, want) <= TOL
+    assert np.array_equal(got, want)  # bit-exact: same order, no FMA
+    st.execute_unfused()
+    assert np.array_equal(st.collect_outputs(), want)
+
+
+def test_config5_batch_full_size(orc):
+    nsys = 8
+    M, vals = sf.config5_systems(nsys=nsys)
+    n, nnz = M.n, M.nnz
+    vin = np.concatenate([sf.gen_vector(n, 7 + s) for s in range(nsys)])
+    for combo in (8, 1):
+        st = sf.make_state(combo, M, nsys=nsys, values=vals, vin=vin)
+        st.execute_fused()
+        got = st.collect_outputs().reshape(nsys, 2 * n)
+        for s in (0, nsys - 1):
+            Ms = Csc(n, M.colptr, M.rowidx, vals[s * nnz:(s + 1) * nnz])
+            want = orc.run_sequential(combo, Ms, 7, vin=vin[s * n:(s + 1) * n])
+            assert max_rel(got[s], want) <= TOL
+            assert np.array_equal(got[s], want)
+        del st
+
+
+def test_config1_residuals():
+    # ||L z - b||_inf / ||b||_inf (SPEC.md:132 bound 1e-12) and y = A z
+    M = sf.config_matrix(1)
+    st = sf.make_state(4, M, seed=7)
+    st.execute_fused()
+    out = st.collect_outputs()
+    n = M.n
+    z, y = out[:n], out[n:]
+    b = sf.gen_vector(n, 7)
+    import scipy.sparse as sp
+    A = sp.csc_matrix((M.values, M.rowidx, M.colptr), shape=(n, n))
+    L = sp.tril(A).tocsr()
+    assert np.max(np.abs(L @ z - b)) <= 1e-12 * np.max(np.abs(b))
+    assert np.max(np.abs(A @ z - y)) <= 1e-12 * max(1, np.max(np.abs(y)))
