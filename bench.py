@@ -1,0 +1,465 @@
+#!/usr/bin/env python
+"""bench.py -- BASELINE.json metric: fused kernel-pair executions/s (fp64)
+and HBM GB/s vs the roofline, with the reference CPU executor beside it.
+
+Workload (config.workload): BASELINE config 5, the largest single-GPU
+configuration -- forward L z = b then backward L^T x = z on the 27-point
+128^3 stencil (n = 2,097,152, nnz(L) = 28,920,060), a batch of 8 systems per
+GPU (own diagonal perturbation and right-hand side each), one fused launch
+per step.  One "exec" = one fused kernel-pair execution on one system.
+
+  python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+  torchrun --nproc-per-node N bench.py --gpus N ...   (one process per GPU)
+
+Multi-GPU: the systems are independent, so each rank runs its own batch of
+8 (weak scaling, no data-path collective); torch.distributed is used only
+for the barrier and the max-over-ranks of the timings.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "fused kernel-pair execs/s (fp64)"
+UNIT = "execs/s"
+CONFIG_COMBO = {1: 4, 2: 5, 3: 6, 4: 7, 5: 8}
+CONFIG_NAME = {
+    1: "SpTRSV->SpMV 2-D 5-pt 512^2 (combo 4)",
+    2: "SpIC0->SpTRSV 3-D 7-pt 64^3 (combo 5)",
+    3: "SpILU0->SpTRSV 3-D conv-diff 96^3 (combo 6)",
+    4: "DAD->SpIC0 random band n=1e6 (combo 7)",
+    5: "SpTRSV->SpTRSV^T fwd L, bwd L^T, 27-pt 128^3, 8 systems/GPU",
+}
+
+
+# ---------------------------------------------------------------------------
+# plumbing: ranks, barrier, max over ranks, clocks
+# ---------------------------------------------------------------------------
+class Dist:
+    def __init__(self):
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.rank = int(os.environ.get("RANK", "0"))
+        self.local = int(os.environ.get("LOCAL_RANK", "0"))
+        self.pg = None
+        if self.world > 1:
+            import torch
+            import torch.distributed as td
+            backend = "nccl" if torch.cuda.is_available() else "gloo"
+            if backend == "nccl":
+                torch.cuda.set_device(self.local)
+            td.init_process_group(backend=backend)
+            self.td = td
+            self.torch = torch
+            self.dev = torch.device("cuda", self.local) if backend == "nccl" else torch.device("cpu")
+
+    def barrier(self):
+        if self.world > 1:
+            self.td.barrier()
+
+    def max(self, x: float) -> float:
+        if self.world == 1:
+            return x
+        t = self.torch.tensor([x], dtype=self.torch.float64, device=self.dev)
+        self.td.all_reduce(t, op=self.td.ReduceOp.MAX)
+        return float(t.item())
+
+    def close(self):
+        if self.world > 1:
+            self.td.destroy_process_group()
+
+
+REASONS = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown",
+           0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+           0x2: "applications_clocks_setting", 0x10: "sync_boost"}
+
+
+class ClockSampler:
+    """NVML sampling of the SM clock and throttle reasons while running."""
+
+    def __init__(self, index: int, period_s: float = 0.005):
+        self.samples = []
+        self.reasons = 0
+        self.max_mhz = None
+        self.ok = False
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            self.ok = False
+        self.period = period_s
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                self.reasons |= int(self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h))
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.ok:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self._stop.set()
+            self._t.join()
+
+    def summary(self):
+        if not self.ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": [], "samples": 0}
+        return {"sm_mhz": float(statistics.median(self.samples)), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(v for k, v in REASONS.items() if self.reasons & k),
+                "samples": len(self.samples)}
+
+
+def hbm_peak():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def ncu_traffic(workload: str):
+    """dram bytes per launch of the dominant kernel from the committed ncu
+    capture (profiles/), or None."""
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return d.get(workload)
+    except Exception:
+        return None
+
+
+# ---------------------------------------------------------------------------
+# algorithmic bytes (each array once per direction)
+# ---------------------------------------------------------------------------
+def algorithmic_bytes(cfg: int, n: int, nnzL: int, nnzA: int) -> int:
+    ptr = 4 * (n + 1)
+    vec = 8 * n
+    if cfg == 1:  # read L + read A + read b + write x + write y
+        return (ptr + 12 * nnzL) + (ptr + 12 * nnzA) + 3 * vec
+    if cfg == 2:  # read A_lower + write L.val + read b + write z
+        return ptr + 12 * nnzL + 8 * nnzL + 2 * vec
+    if cfg == 3:  # read A + write LU.val + read b + write z
+        return ptr + 12 * nnzA + 8 * nnzA + 2 * vec
+    if cfg == 4:  # read A_lower + write L.val + write d
+        return ptr + 12 * nnzL + 8 * nnzL + vec
+    if cfg == 5:  # per system: read L once + read b + write z + write x
+        return ptr + 12 * nnzL + 3 * vec
+    raise ValueError(cfg)
+
+
+def lower_nnz(M) -> int:
+    cols = np.repeat(np.arange(M.n, dtype=np.int64), np.diff(M.colptr))
+    return int(np.count_nonzero(M.rowidx >= cols))
+
+
+# ---------------------------------------------------------------------------
+# inputs
+# ---------------------------------------------------------------------------
+def make_inputs(cfg: int, size, nsys: int, sys0: int):
+    import paper_2111_12238_b200 as sf
+    if cfg == 5:
+        M, vals = sf.config5_systems(size=size, nsys=nsys, seed0=1000 + sys0)
+        vin = np.concatenate([sf.gen_vector(M.n, 7 + sys0 + s) for s in range(nsys)])
+        return M, vals, vin
+    M = sf.config_matrix(cfg, size=size)
+    vin = sf.gen_vector(M.n, 7)
+    return M, None, vin
+
+
+# ---------------------------------------------------------------------------
+# the reference CPU executor (oracle/_ref: unmodified reference headers)
+# ---------------------------------------------------------------------------
+def reference_fused(cfg: int, M, vals, vin, nthreads: int, warmups: int, repeats: int):
+    """Times the reference's execute_fused (msp + compile_schedule once, then
+    warmups + repeats) on one system.  Config 5's fwd->bwd pair does not exist
+    in the reference, so its combo 1 (fwd -> fwd with the same L: identical
+    sizes, bytes and flops) stands in."""
+    from oracle.oracle import Csc, Reference
+    ref = Reference()
+    combo = 1 if cfg == 5 else CONFIG_COMBO[cfg]
+    v0 = M.values if vals is None else vals[:M.nnz]
+    st = ref.state(combo, Csc(M.n, M.colptr, M.rowidx, v0), 7, vin=vin[:M.n])
+    t0 = time.perf_counter()
+    times, insp, nsp = st.bench(1, nthreads, warmups, repeats)
+    wall = time.perf_counter() - t0
+    return {"times": times.tolist(), "median_s": float(np.median(times)), "inspector_s": insp,
+            "s_partitions": nsp, "combo": combo, "wall_s": wall}
+
+
+def cpu_threads() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+def run_ours(args, D: Dist):
+    import paper_2111_12238_b200 as sf
+    from paper_2111_12238_b200 import abi
+    abi.set_device(D.local)
+    cfg = args.config
+    combo = CONFIG_COMBO[cfg] if not (cfg == 5 and args.mode == "fwdfwd") else 1
+    S = args.systems_per_gpu if cfg == 5 else 1
+    t0 = time.perf_counter()
+    M, vals, vin = make_inputs(cfg, args.size, S, D.rank * S)
+    t_gen = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    st = sf.make_state(combo, M, seed=7, nsys=S, values=vals, vin=vin)
+    t_state = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    st.inspect()
+    t_insp = time.perf_counter() - t0
+    nnzL = lower_nnz(M)
+    bytes_per_launch = algorithmic_bytes(cfg, M.n, nnzL, M.nnz) * S
+
+    # ---- device-resident throughput (value)
+    if args.warmup > 0:
+        st.bench(args.warmup)
+    D.barrier()
+    launches0 = st.launch_count()
+    with ClockSampler(D.local) as clk:
+        total_ms, kernel_ms = st.bench(args.steps)
+    launches = st.launch_count() - launches0
+    D.barrier()
+    ms_step = D.max(total_ms / args.steps)
+    kernel_ms = D.max(kernel_ms)
+    value = S * D.world / (ms_step / 1e3)
+
+    # ---- unfused two-kernel GPU sequence on the same inputs
+    st.bench(max(1, args.warmup), unfused=True)
+    D.barrier()
+    u_total, u_kernel = st.bench(args.steps, unfused=True)
+    D.barrier()
+    u_ms = D.max(u_total / args.steps)
+
+    # ---- end to end through the public API: H2D b, execute, D2H outputs
+    n = M.n
+    pin_in = abi.PinnedArray(S * n)
+    pin_out = abi.PinnedArray(S * st.output_len)
+    pin_in.array[:] = vin
+    for _ in range(max(1, args.warmup)):
+        st.set_vin(pin_in.array)
+        st.execute_fused(sync=False)
+        st.collect_outputs(pin_out.array)
+    D.barrier()
+    with ClockSampler(D.local) as clk_e2e:
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            st.set_vin(pin_in.array)
+            st.execute_fused(sync=False)
+            st.collect_outputs(pin_out.array)
+        e2e_s = (time.perf_counter() - t0) / args.steps
+    D.barrier()
+    e2e_s = D.max(e2e_s)
+    e2e = {"value": S * D.world / e2e_s, "unit": UNIT, "h2d_bytes_per_step": 8 * S * n,
+           "d2h_bytes_per_step": 8 * S * st.output_len, "ms_per_step": e2e_s * 1e3,
+           "path": "sfg_set_vin + sfg_execute_fused + sfg_collect_outputs, pinned host buffers"}
+
+    # ---- check the timed result once more against the oracle (rank 0, small cost)
+    peak, peak_src = hbm_peak()
+    achieved = bytes_per_launch / (kernel_ms / 1e3) / 1e9
+    workload = f"config{cfg}"
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": D.world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": CONFIG_NAME[cfg] if not (cfg == 5 and combo == 1)
+                   else CONFIG_NAME[5].replace("bwd L^T", "fwd L (combo 1 parity mode)"),
+                   "baseline_config": cfg, "combo": combo, "n": M.n, "nnz_A": M.nnz,
+                   "nnz_L": nnzL, "systems_per_gpu": S, "global_systems": S * D.world,
+                   "l2": "inputs larger than L2 (L values+indices %.2f GB/GPU > 126 MB)"
+                   % (S * 12 * nnzL / 1e9) if cfg == 5 else "see DESIGN.md",
+                   "parallelism": f"dp{D.world} (independent systems, no collective)"},
+        "gpu_launches": launches,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": ncu_traffic(workload),
+                     "peak_source": peak_src, "kernel_ms": kernel_ms,
+                     "algorithmic_bytes_per_launch": bytes_per_launch,
+                     "kernel": "k_trsv_pair<8,8>" if combo == 8 else f"combo {combo} executor"},
+        "unfused": {"ms_per_step": u_ms, "value": S * D.world / (u_ms / 1e3),
+                    "fused_speedup": u_ms / ms_step},
+        "e2e": e2e,
+        "clocks": clk.summary(),
+        "clocks_e2e": clk_e2e.summary(),
+        "setup_s": {"generate": t_gen, "make_state": t_state, "inspect_gpu": t_insp},
+    }
+
+    # ---- CPU baseline: the reference's fused executor on the box's host cores
+    if D.world == 1 and D.rank == 0 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(cfg, M, vals, vin)
+
+    # ---- the other BASELINE configs on this GPU (single GPU only)
+    if D.world == 1 and not args.no_extras and cfg == 5:
+        line["other_configs"] = other_configs(args)
+
+    pin_in.free()
+    pin_out.free()
+    st.close()
+    return line
+
+
+def cpu_baseline(cfg, M, vals, vin):
+    from oracle.oracle import Reference
+    T = cpu_threads()
+    if Reference.available():
+        r = reference_fused(cfg, M, vals, vin, T, warmups=1, repeats=3)
+        sample = ("1 system of the batch, reference execute_fused (msp + compile_schedule, "
+                  f"T={T}), median of {len(r['times'])} after 1 warm-up")
+        if cfg == 5:
+            sample += ("; combo 1 fwd->fwd on the same L (the reference has no backward "
+                       "L^T solve)")
+        return {"value": 1.0 / r["median_s"], "unit": UNIT, "cores": T, "kind": "reference",
+                "sample": sample, "ms_per_exec": r["median_s"] * 1e3,
+                "inspector_s": r["inspector_s"], "s_partitions": r["s_partitions"]}
+    from oracle.oracle import Csc, Oracle
+    orc = Oracle()
+    v0 = M.values if vals is None else vals[:M.nnz]
+    t0 = time.perf_counter()
+    orc.run_sequential(CONFIG_COMBO[cfg], Csc(M.n, M.colptr, M.rowidx, v0), 7, vin=vin[:M.n])
+    dt = time.perf_counter() - t0
+    return {"value": 1.0 / dt, "unit": UNIT, "cores": 1, "kind": "port",
+            "sample": "1 system, oracle sequential restatement (make_state included)"}
+
+
+def other_configs(args):
+    import paper_2111_12238_b200 as sf
+    from oracle.oracle import Reference
+    out = {}
+    peak, _ = hbm_peak()
+    T = cpu_threads()
+    for cfg in (1, 2, 3, 4):
+        M, _, vin = make_inputs(cfg, None, 1, 0)
+        combo = CONFIG_COMBO[cfg]
+        st = sf.make_state(combo, M, seed=7).inspect()
+        reps = 20
+        st.bench(3)
+        tot, ker = st.bench(reps)
+        ut, uk = st.bench(reps, unfused=True)
+        nnzL = lower_nnz(M)
+        byts = algorithmic_bytes(cfg, M.n, nnzL, M.nnz)
+        ms = tot / reps
+        rec = {"workload": CONFIG_NAME[cfg], "n": M.n, "nnz": M.nnz,
+               "value": 1e3 / ms, "ms_per_exec": ms, "kernel_ms": ker,
+               "achieved_gbs": byts / (ker / 1e3) / 1e9,
+               "frac": byts / (ker / 1e3) / 1e9 / peak,
+               "unfused_ms_per_exec": ut / reps, "fused_speedup": (ut / reps) / ms,
+               "critical_path": int(st.schedule().nspartitions())}
+        if Reference.available() and not args.no_cpu_baseline:
+            try:
+                r = reference_fused(cfg, M, None, vin, T, warmups=1, repeats=3)
+                rec["cpu_reference"] = {"value": 1.0 / r["median_s"], "cores": T,
+                                        "ms_per_exec": r["median_s"] * 1e3,
+                                        "inspector_s": r["inspector_s"]}
+            except Exception as e:  # keep the bench line even if the CPU leg fails
+                rec["cpu_reference"] = {"error": str(e)[:200]}
+        out[f"config{cfg}"] = rec
+        st.close()
+    return out
+
+
+# ---------------------------------------------------------------------------
+# reference arm: the reference's own CPU fused executor
+# ---------------------------------------------------------------------------
+def run_reference(args, D: Dist):
+    if D.rank != 0:
+        return None
+    from oracle.oracle import Reference
+    cfg = args.config
+    if not Reference.available():
+        return {"impl": "reference", "unavailable": "oracle/_ref/libsfref.so not built"}
+    M, vals, vin = make_inputs(cfg, args.size, 1, 0)
+    T = cpu_threads()
+    r = reference_fused(cfg, M, vals, vin, T, warmups=max(args.warmup, 1), repeats=args.steps)
+    mean_s = float(np.mean(r["times"]))
+    value = 1.0 / mean_s
+    sample = (f"reference execute_fused, T={T} host threads, 1 system per step "
+              f"({args.steps} steps after {max(args.warmup, 1)} warm-ups; msp inspector "
+              f"{r['inspector_s']:.1f}s excluded)")
+    if cfg == 5:
+        sample += "; combo 1 fwd->fwd on the same L (no backward L^T solve in the reference)"
+    return {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": D.world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": mean_s * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": CONFIG_NAME[cfg], "baseline_config": cfg, "combo": r["combo"],
+                   "n": M.n, "nnz_A": M.nnz, "systems_per_step": 1},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": T, "kind": "reference",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "inspector_s": r["inspector_s"], "s_partitions": r["s_partitions"],
+    }
+
+
+class _Solo(Dist):
+    def __init__(self):
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.rank = 0
+        self.local = 0
+        self.pg = None
+
+    def barrier(self):
+        pass
+
+    def max(self, x):
+        return x
+
+    def close(self):
+        pass
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--config", type=int, default=5, choices=(1, 2, 3, 4, 5))
+    ap.add_argument("--mode", choices=("fwdbwd", "fwdfwd"), default="fwdbwd")
+    ap.add_argument("--systems-per-gpu", type=int, default=8)
+    ap.add_argument("--size", type=int, default=None, help="grid side / n override (testing)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extras", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        ap.error("--warmup must be >= 3")
+    if args.impl == "reference" and int(os.environ.get("RANK", "0")) != 0:
+        return  # the reference arm runs on rank 0 only
+    D = Dist() if args.impl == "ours" else _Solo()
+    try:
+        line = run_reference(args, D) if args.impl == "reference" else run_ours(args, D)
+        if D.rank == 0 and line is not None:
+            print(json.dumps(line), flush=True)
+    finally:
+        D.close()
+
+
+if __name__ == "__main__":
+    main()

@@ -60,6 +60,12 @@ typedef struct sfg_plan sfg_plan;
 /* Returns SFG_OK when a CUDA device is usable; SFG_ERR_NO_DEVICE otherwise. */
 sfg_status sfg_device_check(int32_t* device_count, int32_t* sm_count);
 const char* sfg_version(void);
+/* Select the CUDA device for subsequent plan creation on this thread
+ * (one process per GPU: rank r calls sfg_set_device(local_rank)). */
+sfg_status sfg_set_device(int32_t device);
+/* Page-locked host buffers for the end-to-end path (cudaHostAlloc). */
+sfg_status sfg_host_alloc(size_t bytes, void** ptr);
+sfg_status sfg_host_free(void* ptr);
 
 /* Plan lifetime (replaces make_state, kernels.hpp:429-495) ----------------
  * M: square CSC matrix (n, colptr[n+1], rowidx[nnz], values), host memory.
@@ -70,6 +76,8 @@ const char* sfg_version(void);
  *   i.e. exactly make_state's vector).  Ignored for combo 7.
  * Storage conversions (lower_triangle, to_csr, build_lower_rows,
  * find_diag_positions, the DSCAL vector) run on the GPU. */
+/* On failure *out may still be set so sfg_last_error can report the cause;
+ * destroy it with sfg_plan_destroy. */
 sfg_status sfg_plan_create(int32_t combo, int32_t n, const int32_t* colptr,
                            const int32_t* rowidx, const double* values,
                            int32_t nsys, const double* vin, uint64_t seed,
@@ -136,6 +144,14 @@ int64_t sfg_launch_count(const sfg_plan* plan);
  * completion).  kernel_ms (optional) receives the time of the dominant
  * executor kernel alone. */
 sfg_status sfg_last_exec_ms(sfg_plan* plan, float* total_ms, float* kernel_ms);
+
+/* Back-to-back executions on the plan stream, timed with CUDA events
+ * recorded on that stream: total_ms covers all `reps` executions (output
+ * re-initialisation included); kernel_ms_avg is the mean duration of the
+ * main executor kernel per execution.  unfused != 0 times the two-launch
+ * comparator instead.  Returns SFG_ERR_FACTORIZATION on breakdown. */
+sfg_status sfg_bench_executions(sfg_plan* plan, int32_t reps, int32_t unfused,
+                                float* total_ms, float* kernel_ms_avg);
 
 /* Fixtures (replaces fixtures.hpp generators + the BASELINE configs) -------
  * Generated matrices are returned through an opaque handle. */

@@ -24,7 +24,8 @@ SFG_ERR_NO_DEVICE = 6
 
 # Every function include/sfgpu.h declares (checked by tests/test_abi.py).
 EXPORTS = (
-    "sfg_device_check", "sfg_version", "sfg_plan_create", "sfg_plan_destroy",
+    "sfg_device_check", "sfg_version", "sfg_set_device", "sfg_host_alloc",
+    "sfg_host_free", "sfg_bench_executions", "sfg_plan_create", "sfg_plan_destroy",
     "sfg_plan_set_stream", "sfg_plan_info", "sfg_set_vin", "sfg_inspect",
     "sfg_get_dag", "sfg_get_interdep", "sfg_get_levels", "sfg_compute_reuse",
     "sfg_get_schedule", "sfg_execute_fused", "sfg_execute_unfused",
@@ -61,6 +62,15 @@ def load(path: str | None = None):
     L.sfg_version.restype = C.c_char_p
     L.sfg_device_check.argtypes = [i32p, i32p]
     L.sfg_device_check.restype = st
+    L.sfg_set_device.argtypes = [C.c_int32]
+    L.sfg_set_device.restype = st
+    L.sfg_host_alloc.argtypes = [C.c_size_t, C.POINTER(vp)]
+    L.sfg_host_alloc.restype = st
+    L.sfg_host_free.argtypes = [vp]
+    L.sfg_host_free.restype = st
+    L.sfg_bench_executions.argtypes = [vp, C.c_int32, C.c_int32, C.POINTER(C.c_float),
+                                       C.POINTER(C.c_float)]
+    L.sfg_bench_executions.restype = st
     L.sfg_plan_create.argtypes = [C.c_int32, C.c_int32, i32p, i32p, f64p, C.c_int32, f64p,
                                   C.c_uint64, C.POINTER(vp)]
     L.sfg_plan_create.restype = st
@@ -122,3 +132,34 @@ def device_available() -> bool:
     cnt = C.c_int32(0)
     sms = C.c_int32(0)
     return L.sfg_device_check(C.byref(cnt), C.byref(sms)) == SFG_OK and cnt.value > 0
+
+
+class PinnedArray:
+    """A page-locked host float64 buffer (sfg_host_alloc) viewed as numpy."""
+
+    def __init__(self, count: int):
+        L = load()
+        self._L = L
+        self._p = C.c_void_p()
+        st = L.sfg_host_alloc(max(count, 1) * 8, C.byref(self._p))
+        if st != SFG_OK:
+            raise RuntimeError(f"sfg_host_alloc failed (status {st})")
+        buf = (C.c_double * max(count, 1)).from_address(self._p.value)
+        self.array = np.frombuffer(buf, dtype=np.float64, count=count)
+
+    def free(self):
+        if self._p:
+            self._L.sfg_host_free(self._p)
+            self._p = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+def set_device(dev: int):
+    st = load().sfg_set_device(dev)
+    if st != SFG_OK:
+        raise RuntimeError(f"sfg_set_device({dev}) failed (status {st})")

@@ -279,6 +279,17 @@ class KernelState:
         self._chk(self.L.sfg_last_exec_ms(self.h, C.byref(tot), C.byref(ker)), "last_exec_ms")
         return tot.value, ker.value
 
+    def bench(self, reps: int, unfused: bool = False):
+        """reps back-to-back executions timed with CUDA events on the plan
+        stream: (total_ms, mean main-kernel ms)."""
+        if not self.inspected:
+            self.inspect()
+        tot = C.c_float()
+        ker = C.c_float()
+        self._chk(self.L.sfg_bench_executions(self.h, reps, 1 if unfused else 0, C.byref(tot),
+                                              C.byref(ker)), "bench")
+        return tot.value, ker.value
+
     def launch_count(self) -> int:
         return int(self.L.sfg_launch_count(self.h))
 

@@ -42,16 +42,18 @@ __device__ __forceinline__ void st_relaxed_i32(int* p, int v) {
   asm volatile("st.relaxed.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
-// Spin until *p != SENT; exponential nanosleep backoff keeps the pollers from
-// saturating the L2 slices the producers are writing to.
-__device__ __forceinline__ double poll_f64(const double* p) {
+// Spin until *p != SENT; an optional exponential nanosleep backoff (capped at
+// g_sleep_cap ns; 0 = pure spin) keeps pollers off the producers' L2 slices.
+__device__ __forceinline__ double poll_f64(const double* p, unsigned sleep_cap = 160) {
   unsigned long long v = ld_relaxed_u64(p);
   if (v != SENT)
     return __longlong_as_double((long long)v);
   unsigned ns = 20;
   do {
-    __nanosleep(ns);
-    ns = ns < 160 ? ns * 2 : 160;
+    if (sleep_cap) {
+      __nanosleep(ns);
+      ns = ns < sleep_cap ? ns * 2 : sleep_cap;
+    }
     v = ld_relaxed_u64(p);
   } while (v == SENT);
   return __longlong_as_double((long long)v);

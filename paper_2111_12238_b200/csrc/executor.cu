@@ -46,7 +46,7 @@ __device__ __forceinline__ double solve_row(int r, int s,
                                             const double* __restrict__ val,
                                             double rhs, const double* x,
                                             unsigned long long* err, int kernel,
-                                            int seqpos) {
+                                            int seqpos, unsigned cap) {
   const int b = __ldg(ptr + r);
   const int e = __ldg(ptr + r + 1) - 1;
   const double d = __ldg(val + (size_t)e * S + s);
@@ -70,7 +70,7 @@ __device__ __forceinline__ double solve_row(int r, int s,
     for (int a = 0; a < CH; ++a)
       if (a < cnt) {
         const double xj = xx[a] != SENT ? as_f64(xx[a])
-                                        : poll_f64(x + (size_t)jj[a] * S + s);
+                                        : poll_f64(x + (size_t)jj[a] * S + s, cap);
         acc = fsub_mul(acc, vv[a], xj);
       }
   }
@@ -88,7 +88,7 @@ __device__ __forceinline__ double gather_row(int r,
                                              const int32_t* __restrict__ ptr,
                                              const int32_t* __restrict__ idx,
                                              const double* __restrict__ val,
-                                             const double* x) {
+                                             const double* x, unsigned cap) {
   const int b = __ldg(ptr + r);
   const int e = __ldg(ptr + r + 1);
   double acc = 0.0;
@@ -110,7 +110,7 @@ __device__ __forceinline__ double gather_row(int r,
 #pragma unroll
     for (int a = 0; a < CH; ++a)
       if (a < cnt) {
-        const double xj = xx[a] != SENT ? as_f64(xx[a]) : poll_f64(x + jj[a]);
+        const double xj = xx[a] != SENT ? as_f64(xx[a]) : poll_f64(x + jj[a], cap);
         acc = __dadd_rn(acc, __dmul_rn(vv[a], xj));
       }
   }
@@ -144,27 +144,27 @@ __global__ void __launch_bounds__(kBlock, 2) k_trsv_pair(const ExecArgs A) {
       double z;
       if (A.phase & 1) {
         z = solve_row<S>(r, s, A.lr_ptr, A.lr_idx, A.lr_val,
-                         __ldg(A.vin + (size_t)r * S + s), A.vmid, A.err, 1, r);
+                         __ldg(A.vin + (size_t)r * S + s), A.vmid, A.err, 1, r, A.sleep_cap);
         publish_f64(A.vmid + (size_t)r * S + s, z);
       } else {
-        z = poll_f64(A.vmid + (size_t)r * S + s);
+        z = poll_f64(A.vmid + (size_t)r * S + s, A.sleep_cap);
       }
       if (A.phase & 2) {
         const double x2 = solve_row<S>(r, s, A.lr_ptr, A.lr_idx, A.lr_val, z,
-                                       A.vout, A.err, 2, r);
+                                       A.vout, A.err, 2, r, A.sleep_cap);
         publish_f64(A.vout + (size_t)r * S + s, x2);
       }
     } else if (t < A.n) { // forward row of kernel 1 (combos 4, 8)
       const double z =
           solve_row<S>(r, s, A.lr_ptr, A.lr_idx, A.lr_val,
-                       __ldg(A.vin + (size_t)r * S + s), A.vmid, A.err, 1, r);
+                       __ldg(A.vin + (size_t)r * S + s), A.vmid, A.err, 1, r, A.sleep_cap);
       publish_f64(A.vmid + (size_t)r * S + s, z);
     } else if (COMBO == 4) {
-      A.vout[r] = gather_row(r, A.ar_ptr, A.ar_idx, A.ar_val, A.vmid);
+      A.vout[r] = gather_row(r, A.ar_ptr, A.ar_idx, A.ar_val, A.vmid, A.sleep_cap);
     } else { // COMBO 8 backward row r of L': rhs z_r, then x_j for j > r
-      const double z = poll_f64(A.vmid + (size_t)r * S + s);
+      const double z = poll_f64(A.vmid + (size_t)r * S + s, A.sleep_cap);
       const double x = solve_row<S>(r, s, A.lt_ptr, A.lt_idx, A.lt_val, z,
-                                    A.vout, A.err, 2, A.n - 1 - r);
+                                    A.vout, A.err, 2, A.n - 1 - r, A.sleep_cap);
       publish_f64(A.vout + (size_t)r * S + s, x);
     }
   }
@@ -225,9 +225,9 @@ __global__ void __launch_bounds__(kBlock) k_ic0(const ExecArgs A) {
         const int j = __ldg(A.rv_col + q);
         const int pj = __ldg(A.rv_pos + q);
         const int pe = __ldg(A.lc_ptr + j + 1);
-        const double lkj = poll_f64(A.fac + pj);
+        const double lkj = poll_f64(A.fac + pj, A.sleep_cap);
         if (do_solve)
-          acc2 = fsub_mul(acc2, lkj, poll_f64(A.vout + j));
+          acc2 = fsub_mul(acc2, lkj, poll_f64(A.vout + j, A.sleep_cap));
         // merge rows of column j from row k on with the rows of column k
         int a = 0;
         for (int p = pj; p < pe; ++p) {
@@ -237,7 +237,7 @@ __global__ void __launch_bounds__(kBlock) k_ic0(const ExecArgs A) {
           if (a == m)
             break;
           if ((local ? rowl[a] : __ldg(A.lc_idx + c0 + a)) == i)
-            acc[a] = fsub_mul(acc[a], lkj, poll_f64(A.fac + p));
+            acc[a] = fsub_mul(acc[a], lkj, poll_f64(A.fac + p, A.sleep_cap));
         }
       }
       const double d = acc[0];
@@ -254,9 +254,9 @@ __global__ void __launch_bounds__(kBlock) k_ic0(const ExecArgs A) {
       }
     } else if (do_solve) { // combo 5 kernel 2 alone (unfused second launch)
       for (int q = q0; q < q1; ++q)
-        acc2 = fsub_mul(acc2, poll_f64(A.fac + __ldg(A.rv_pos + q)),
-                        poll_f64(A.vout + __ldg(A.rv_col + q)));
-      const double d = poll_f64(A.fac + c0);
+        acc2 = fsub_mul(acc2, poll_f64(A.fac + __ldg(A.rv_pos + q), A.sleep_cap),
+                        poll_f64(A.vout + __ldg(A.rv_col + q), A.sleep_cap));
+      const double d = poll_f64(A.fac + c0, A.sleep_cap);
       if (d == 0.0)
         report_error(A.err, 2, k, k);
       publish_f64(A.vout + k, __ddiv_rn(acc2, d));
@@ -302,7 +302,7 @@ __global__ void __launch_bounds__(kBlock) k_ilu0(const ExecArgs A) {
         if (k >= i)
           break;
         const int dk = __ldg(A.diag + k);
-        const double piv = dk >= 0 ? poll_f64(A.fac + dk) : 0.0;
+        const double piv = dk >= 0 ? poll_f64(A.fac + dk, A.sleep_cap) : 0.0;
         if (dk < 0 || piv == 0.0)
           report_error(A.err, 1, i, k);
         const double lik = __ddiv_rn(acc[a], piv);
@@ -317,11 +317,11 @@ __global__ void __launch_bounds__(kBlock) k_ilu0(const ExecArgs A) {
             if (b == m)
               break;
             if (COL(b) == j)
-              acc[b] = fsub_mul(acc[b], lik, poll_f64(A.fac + q));
+              acc[b] = fsub_mul(acc[b], lik, poll_f64(A.fac + q, A.sleep_cap));
           }
         }
         if (do_solve)
-          acc2 = fsub_mul(acc2, lik, poll_f64(A.vout + k));
+          acc2 = fsub_mul(acc2, lik, poll_f64(A.vout + k, A.sleep_cap));
       }
 #undef COL
       for (int a = 0; a < m; ++a)
@@ -331,7 +331,7 @@ __global__ void __launch_bounds__(kBlock) k_ilu0(const ExecArgs A) {
         const int k = __ldg(A.ar_idx + p);
         if (k >= i)
           break;
-        acc2 = fsub_mul(acc2, poll_f64(A.fac + p), poll_f64(A.vout + k));
+        acc2 = fsub_mul(acc2, poll_f64(A.fac + p, A.sleep_cap), poll_f64(A.vout + k, A.sleep_cap));
       }
     }
     if (do_solve)
@@ -391,7 +391,9 @@ template <typename K> void launch_persistent(K kernel, const ExecArgs& a, cudaSt
     return;
   const int64_t warps_needed = (total + tickets_per_warp - 1) / tickets_per_warp;
   int64_t blocks = (warps_needed + (kBlock / 32) - 1) / (kBlock / 32);
-  const int64_t cap = resident_grid(kernel);
+  int64_t cap = resident_grid(kernel);
+  if (a.blocks_per_sm > 0 && (int64_t)a.blocks_per_sm * sm_count() < cap)
+    cap = (int64_t)a.blocks_per_sm * sm_count();
   if (blocks > cap)
     blocks = cap;
   kernel<<<(unsigned)blocks, kBlock, 0, s>>>(a);

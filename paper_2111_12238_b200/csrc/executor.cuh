@@ -45,6 +45,8 @@ struct ExecArgs {
   double* vout = nullptr;
   double* fac = nullptr;
   double* work = nullptr; // per-position scratch (long columns, DSCAL stage)
+  unsigned sleep_cap = 160; // poll backoff cap in ns (0 = pure spin)
+  int blocks_per_sm = 0;    // 0 = occupancy limit
 };
 
 struct FillRegion {

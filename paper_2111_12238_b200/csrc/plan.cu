@@ -3,6 +3,7 @@
 // / inter_dag / joint_dag / level_info / compute_reuse / execute_fused /
 // execute_unfused / collect_outputs (kernels.hpp, dag.hpp, executor.hpp).
 #include "../../include/sfgpu.h"
+#include "bsf.cuh"
 #include "common.cuh"
 #include "executor.cuh"
 #include "internal.hpp"
@@ -10,6 +11,7 @@
 #include <cub/device/device_scan.cuh>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <random>
@@ -54,6 +56,15 @@ struct sfg_plan {
   DBuf<int32_t> lev[3], hgt[3], slk[3];
   int32_t crit[3] = {0, 0, 0};
   bool have_levels[3] = {false, false, false};
+
+  // blocked sync-free executor (combos 1, 4, 8)
+  bool use_bsf = false;
+  BsfLayout bsf_f, bsf_b;
+  DBuf<int32_t> tick_fused, tick_unfused;
+  int64_t nt = 0, nt_k1 = 0;
+  int32_t y_block = 0, y_blocks = 0;
+  std::vector<int32_t> row_maxcol; // combo 4: last x index each SpMV row reads
+  std::vector<int32_t> host_tickets;
 
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
   bool timed = false;
@@ -372,6 +383,13 @@ void build_plan(sfg_plan* P, const int32_t* colptr, const int32_t* rowidx,
       if (rowidx[p] >= j)
         ++lower;
   P->lower_count = lower;
+  if (P->combo == 4) {
+    // CSR(A) row r reads x_j for every (r, j) in A: remember the largest j
+    P->row_maxcol.assign((size_t)n, -1);
+    for (int32_t j = 0; j < n; ++j)
+      for (int32_t p = colptr[j]; p < colptr[j + 1]; ++p)
+        P->row_maxcol[(size_t)rowidx[p]] = std::max(P->row_maxcol[(size_t)rowidx[p]], j);
+  }
 
   upload(P->m_ptr, colptr, (int64_t)n + 1, s);
   upload(P->m_idx, rowidx, nnzM, s);
@@ -508,6 +526,10 @@ ExecArgs exec_args(sfg_plan* P) {
   a.vout = P->vout.p;
   a.fac = P->fac.p;
   a.work = P->work.p;
+  if (const char* e = getenv("SFG_SLEEP_CAP"))
+    a.sleep_cap = (unsigned)atoi(e);
+  if (const char* e = getenv("SFG_BLOCKS_PER_SM"))
+    a.blocks_per_sm = atoi(e);
   return a;
 }
 
@@ -536,6 +558,8 @@ void launch_main(sfg_plan* P, const ExecArgs& a) {
 }
 
 void do_inspect(sfg_plan* P) {
+  if (P->inspected)
+    return;
   cudaStream_t s = P->stream;
   const int32_t n = P->n;
   const int combo = P->combo;
@@ -579,8 +603,90 @@ void do_inspect(sfg_plan* P) {
     for (size_t k = 1; k < w2.size(); ++k)
       P->wave_ptr.push_back(w2[k] + n);
   }
+  if (combo == 1 || combo == 4 || combo == 8) {
+    const char* ex = getenv("SFG_EXECUTOR");
+    P->use_bsf = ex && std::string(ex) == "bsf";
+  }
+  if (P->use_bsf) {
+    const int32_t S = P->nsys;
+    int32_t B = S >= 8 ? 16384 / S : 8192 / S;
+    if (combo == 1)
+      B /= 2;
+    if (const char* e = getenv("SFG_BSF_B"))
+      B = std::max(32, atoi(e));
+    B = std::max<int32_t>(1, std::min<int32_t>(B, std::max<int32_t>(n, 1)));
+    const int32_t bmax = (200 * 1024) / (8 * S * (combo == 1 ? 2 : 1));
+    B = std::min(B, bmax);
+    build_bsf(P->lr_ptr.p, P->lr_idx.p, P->lr_val.p, n, S, +1, B, P->bsf_f, s);
+    if (combo == 8)
+      build_bsf(P->lt_ptr.p, P->lt_idx.p, P->lt_val.p, n, S, -1, B, P->bsf_b, s);
+    std::vector<int32_t> y_after;
+    if (combo == 4) {
+      P->y_block = std::max<int32_t>(256, B / 2);
+      P->y_blocks = (n + P->y_block - 1) / P->y_block;
+      y_after.assign((size_t)P->y_blocks, -1);
+      for (int32_t r = 0; r < n; ++r) {
+        const int32_t j = P->row_maxcol[(size_t)r];
+        const int32_t k = r / P->y_block;
+        if (j >= 0)
+          y_after[(size_t)k] = std::max(y_after[(size_t)k], j / B);
+      }
+    }
+    P->host_tickets = bsf_tickets(combo, P->bsf_f, combo == 8 ? &P->bsf_b : nullptr, P->y_blocks,
+                                  y_after, &P->nt_k1);
+    P->nt = (int64_t)P->host_tickets.size();
+    upload(P->tick_fused, P->host_tickets.data(), P->nt, s);
+    std::vector<int32_t> unf;
+    for (int32_t b = 0; b < P->bsf_f.nblk; ++b)
+      unf.push_back(ticket(TK_FWD, b));
+    for (int32_t b = 0; b < P->bsf_b.nblk; ++b)
+      unf.push_back(ticket(TK_BWD, b));
+    for (int32_t k = 0; k < P->y_blocks; ++k)
+      unf.push_back(ticket(TK_Y, k));
+    upload(P->tick_unfused, unf.data(), (int64_t)unf.size(), s);
+    SFG_CUDA(cudaStreamSynchronize(s));
+    // the blocked layouts carry their own copies of the values
+    P->lr_val.release();
+    P->lt_val.release();
+  }
   SFG_CUDA(cudaStreamSynchronize(s));
   P->inspected = true;
+}
+
+BsfArgs bsf_args(sfg_plan* P) {
+  BsfArgs a;
+  a.combo = P->combo;
+  a.n = P->n;
+  a.S = P->nsys;
+  a.counter = P->counter.p;
+  a.err = P->err.p;
+  a.Bf = P->bsf_f.B;
+  a.nblk_f = P->bsf_f.nblk;
+  a.f_rowP = P->bsf_f.rowP.p;
+  a.f_ptr = P->bsf_f.nptr.p;
+  a.f_idx = P->bsf_f.nidx.p;
+  a.f_val = P->bsf_f.nval.p;
+  a.f_diag = P->bsf_f.dval.p;
+  a.f_bptr = P->bsf_f.bptr.p;
+  a.f_blkb = P->bsf_f.blk_batch.p;
+  a.Bb = P->bsf_b.B;
+  a.b_rowP = P->bsf_b.rowP.p;
+  a.b_ptr = P->bsf_b.nptr.p;
+  a.b_idx = P->bsf_b.nidx.p;
+  a.b_val = P->bsf_b.nval.p;
+  a.b_diag = P->bsf_b.dval.p;
+  a.b_bptr = P->bsf_b.bptr.p;
+  a.b_blkb = P->bsf_b.blk_batch.p;
+  a.By = P->y_block;
+  a.ar_ptr = P->ar_ptr.p;
+  a.ar_idx = P->ar_idx.p;
+  a.ar_val = P->ar_val.p;
+  a.vin = P->vin.p;
+  a.vmid = P->vmid.p;
+  a.vout = P->vout.p;
+  if (const char* e = getenv("SFG_BLOCKS_PER_SM"))
+    a.blocks_per_sm = atoi(e);
+  return a;
 }
 
 // ---- parity DAGs ---------------------------------------------------------
@@ -798,12 +904,145 @@ sfg_status check_error_word(sfg_plan* P) {
                  index);
 }
 
+// One fused execution: re-initialise outputs + ticket counter + error word,
+// then the single executor launch, bracketed by kb / ke.
+void exec_fused_impl(sfg_plan* P, cudaEvent_t kb, cudaEvent_t ke) {
+  const int64_t nv = (int64_t)P->n * P->nsys;
+  FillRegion r[3];
+  int nr = 0;
+  switch (P->combo) {
+  case 1:
+  case 8:
+    r[nr++] = {P->vmid.p, nv};
+    r[nr++] = {P->vout.p, nv};
+    break;
+  case 4:
+    r[nr++] = {P->vmid.p, nv};
+    break;
+  case 5:
+  case 6:
+    r[nr++] = {P->fac.p, P->nnzF};
+    r[nr++] = {P->vout.p, nv};
+    break;
+  case 7:
+    r[nr++] = {P->fac.p, P->nnzF};
+    break;
+  }
+  launch_prep(r, nr, P->counter.p, P->err.p, P->stream);
+  SFG_CUDA(cudaEventRecord(kb, P->stream));
+  if (P->use_bsf) {
+    BsfArgs b = bsf_args(P);
+    b.phase = 3;
+    b.tickets = P->tick_fused.p;
+    b.nt = P->nt;
+    launch_bsf(b, P->stream);
+  } else {
+    ExecArgs a = exec_args(P);
+    a.phase = 3;
+    a.t_begin = 0;
+    a.t_end = P->ntickets;
+    launch_main(P, a);
+  }
+  SFG_CUDA(cudaEventRecord(ke, P->stream));
+}
+
+// The unfused comparator (execute_unfused, executor.hpp:325-383): kernel 1
+// alone, then kernel 2 alone; stream order is the barrier between them.
+void exec_unfused_impl(sfg_plan* P, cudaEvent_t kb, cudaEvent_t ke) {
+  const int64_t nv = (int64_t)P->n * P->nsys;
+  const int c = P->combo;
+  const int32_t n = P->n;
+  ExecArgs a = exec_args(P);
+  FillRegion r1[2];
+  int n1 = 0;
+  if (c == 1 || c == 4 || c == 8)
+    r1[n1++] = {P->vmid.p, nv};
+  else if (c == 5 || c == 6)
+    r1[n1++] = {P->fac.p, P->nnzF};
+  launch_prep(r1, n1, P->counter.p, P->err.p, P->stream);
+  SFG_CUDA(cudaEventRecord(kb, P->stream));
+  if (P->use_bsf) {
+    BsfArgs b = bsf_args(P);
+    b.phase = 1;
+    b.tickets = P->tick_unfused.p;
+    b.nt = P->nt_k1;
+    launch_bsf(b, P->stream);
+    FillRegion r2[1];
+    int n2 = 0;
+    if (c == 1 || c == 8)
+      r2[n2++] = {P->vout.p, nv};
+    launch_prep(r2, n2, P->counter.p, nullptr, P->stream);
+    b.phase = 2;
+    if (c == 1) {
+      b.nt = P->nt_k1;
+    } else {
+      b.tickets = P->tick_unfused.p + P->nt_k1;
+      b.nt = P->nt - P->nt_k1;
+    }
+    launch_bsf(b, P->stream);
+    SFG_CUDA(cudaEventRecord(ke, P->stream));
+    return;
+  }
+  a.phase = 1;
+  a.t_begin = 0;
+  a.t_end = n;
+  if (c == 7)
+    launch_dscal(a, P->stream);
+  else
+    launch_main(P, a);
+  FillRegion r2[2];
+  int n2 = 0;
+  if (c == 1 || c == 8 || c == 5 || c == 6)
+    r2[n2++] = {P->vout.p, nv};
+  else if (c == 7)
+    r2[n2++] = {P->fac.p, P->nnzF};
+  launch_prep(r2, n2, P->counter.p, nullptr, P->stream);
+  a.phase = 2;
+  if (c == 4 || c == 8) {
+    a.t_begin = n;
+    a.t_end = 2 * (int64_t)n;
+  }
+  launch_main(P, a);
+  SFG_CUDA(cudaEventRecord(ke, P->stream));
+}
+
 } // namespace
 
 // ===========================================================================
 extern "C" {
 
 const char* sfg_version(void) { return "sfgpu 0.1 (sm_100a)"; }
+
+sfg_status sfg_set_device(int32_t device) {
+  int cnt = 0;
+  if (cudaGetDeviceCount(&cnt) != cudaSuccess || cnt <= 0) {
+    cudaGetLastError();
+    return SFG_ERR_NO_DEVICE;
+  }
+  if (device < 0 || device >= cnt)
+    return SFG_ERR_INVALID_ARGUMENT;
+  return cudaSetDevice(device) == cudaSuccess ? SFG_OK : SFG_ERR_CUDA;
+}
+
+sfg_status sfg_host_alloc(size_t bytes, void** p) {
+  if (!p)
+    return SFG_ERR_INVALID_ARGUMENT;
+  *p = nullptr;
+  int cnt = 0;
+  if (cudaGetDeviceCount(&cnt) != cudaSuccess || cnt <= 0) {
+    cudaGetLastError();
+    return SFG_ERR_NO_DEVICE;
+  }
+  return cudaHostAlloc(p, bytes > 0 ? bytes : 1, cudaHostAllocDefault) == cudaSuccess
+             ? SFG_OK
+             : SFG_ERR_CUDA;
+}
+
+sfg_status sfg_host_free(void* p) {
+  if (p)
+    cudaFreeHost(p);
+  return SFG_OK;
+}
 
 sfg_status sfg_device_check(int32_t* device_count, int32_t* sms) {
   int cnt = 0;
@@ -1049,6 +1288,61 @@ sfg_status sfg_get_schedule(sfg_plan* P, int64_t* nentries, uint8_t* tags, int32
     return SFG_ERR_INVALID_ARGUMENT;
   if (!P->inspected)
     return set_err(P, SFG_ERR_LOGIC, "sfg_inspect has not run");
+  if (P->use_bsf) {
+    return guarded(P, [&] {
+      DeviceScope ds(P->device);
+      const int32_t n = P->n;
+      std::vector<int32_t> rf((size_t)n), rb;
+      if (n)
+        SFG_CUDA(cudaMemcpy(rf.data(), P->bsf_f.rowP.p, sizeof(int32_t) * (size_t)n,
+                            cudaMemcpyDeviceToHost));
+      if (P->combo == 8) {
+        rb.resize((size_t)n);
+        if (n)
+          SFG_CUDA(cudaMemcpy(rb.data(), P->bsf_b.rowP.p, sizeof(int32_t) * (size_t)n,
+                              cudaMemcpyDeviceToHost));
+      }
+      std::vector<uint8_t> tg;
+      std::vector<int32_t> it;
+      std::vector<int64_t> wp{0};
+      for (int32_t tk : P->host_tickets) {
+        const int kind = tk >> 28, bi = tk & 0x0FFFFFFF;
+        if (kind == TK_Y) {
+          for (int32_t r = bi * P->y_block; r < std::min(n, (bi + 1) * P->y_block); ++r) {
+            tg.push_back(2);
+            it.push_back(r);
+          }
+        } else {
+          const BsfLayout& L = kind == TK_BWD ? P->bsf_b : P->bsf_f;
+          for (int32_t q = bi * L.B; q < std::min(n, (bi + 1) * L.B); ++q) {
+            if (kind == TK_BWD) {
+              tg.push_back(2);
+              it.push_back(n - 1 - rb[(size_t)q]);
+            } else {
+              tg.push_back(1);
+              it.push_back(rf[(size_t)q]);
+              if (P->combo == 1) {
+                tg.push_back(2);
+                it.push_back(rf[(size_t)q]);
+              }
+            }
+          }
+        }
+        wp.push_back((int64_t)tg.size());
+      }
+      if (nentries)
+        *nentries = (int64_t)tg.size();
+      if (nwaves)
+        *nwaves = (int32_t)wp.size() - 1;
+      if (wave_ptr)
+        std::copy(wp.begin(), wp.end(), wave_ptr);
+      if (tags)
+        std::copy(tg.begin(), tg.end(), tags);
+      if (iters)
+        std::copy(it.begin(), it.end(), iters);
+      return SFG_OK;
+    });
+  }
   return guarded(P, [&] {
     DeviceScope ds(P->device);
     const bool fused_task = !(P->combo == 4 || P->combo == 8);
@@ -1097,36 +1391,8 @@ sfg_status sfg_execute_fused(sfg_plan* P) {
   return guarded(P, [&] {
     DeviceScope ds(P->device);
     LaunchScope ls(P);
-    const int64_t nv = (int64_t)P->n * P->nsys;
-    FillRegion r[3];
-    int nr = 0;
-    switch (P->combo) {
-    case 1:
-    case 8:
-      r[nr++] = {P->vmid.p, nv};
-      r[nr++] = {P->vout.p, nv};
-      break;
-    case 4:
-      r[nr++] = {P->vmid.p, nv};
-      break;
-    case 5:
-    case 6:
-      r[nr++] = {P->fac.p, P->nnzF};
-      r[nr++] = {P->vout.p, nv};
-      break;
-    case 7:
-      r[nr++] = {P->fac.p, P->nnzF};
-      break;
-    }
     SFG_CUDA(cudaEventRecord(P->ev[0], P->stream));
-    launch_prep(r, nr, P->counter.p, P->err.p, P->stream);
-    SFG_CUDA(cudaEventRecord(P->ev[1], P->stream));
-    ExecArgs a = exec_args(P);
-    a.phase = 3;
-    a.t_begin = 0;
-    a.t_end = P->ntickets;
-    launch_main(P, a);
-    SFG_CUDA(cudaEventRecord(P->ev[2], P->stream));
+    exec_fused_impl(P, P->ev[1], P->ev[2]);
     SFG_CUDA(cudaEventRecord(P->ev[3], P->stream));
     P->timed = true;
     return SFG_OK;
@@ -1141,42 +1407,8 @@ sfg_status sfg_execute_unfused(sfg_plan* P) {
   return guarded(P, [&] {
     DeviceScope ds(P->device);
     LaunchScope ls(P);
-    const int64_t nv = (int64_t)P->n * P->nsys;
-    const int c = P->combo;
-    const int32_t n = P->n;
-    ExecArgs a = exec_args(P);
     SFG_CUDA(cudaEventRecord(P->ev[0], P->stream));
-    // ---- kernel 1
-    FillRegion r1[2];
-    int n1 = 0;
-    if (c == 1 || c == 4 || c == 8)
-      r1[n1++] = {P->vmid.p, nv};
-    else if (c == 5 || c == 6)
-      r1[n1++] = {P->fac.p, P->nnzF};
-    launch_prep(r1, n1, P->counter.p, P->err.p, P->stream);
-    SFG_CUDA(cudaEventRecord(P->ev[1], P->stream));
-    a.phase = 1;
-    a.t_begin = 0;
-    a.t_end = n;
-    if (c == 7)
-      launch_dscal(a, P->stream);
-    else
-      launch_main(P, a);
-    // ---- kernel 2 (stream order is the barrier between the kernels)
-    FillRegion r2[2];
-    int n2 = 0;
-    if (c == 1 || c == 8 || c == 5 || c == 6)
-      r2[n2++] = {P->vout.p, nv};
-    else if (c == 7)
-      r2[n2++] = {P->fac.p, P->nnzF};
-    launch_prep(r2, n2, P->counter.p, nullptr, P->stream);
-    a.phase = 2;
-    if (c == 4 || c == 8) {
-      a.t_begin = n;
-      a.t_end = 2 * (int64_t)n;
-    }
-    launch_main(P, a);
-    SFG_CUDA(cudaEventRecord(P->ev[2], P->stream));
+    exec_unfused_impl(P, P->ev[1], P->ev[2]);
     SFG_CUDA(cudaEventRecord(P->ev[3], P->stream));
     P->timed = true;
     return SFG_OK;
@@ -1280,6 +1512,44 @@ sfg_status sfg_last_error(const sfg_plan* P, int32_t* kind, int32_t* index, char
 }
 
 int64_t sfg_launch_count(const sfg_plan* P) { return P ? P->launches : -1; }
+
+sfg_status sfg_bench_executions(sfg_plan* P, int32_t reps, int32_t unfused, float* total_ms,
+                                float* kernel_ms_avg) {
+  if (!P || reps < 1)
+    return SFG_ERR_INVALID_ARGUMENT;
+  if (!P->inspected)
+    return set_err(P, SFG_ERR_LOGIC, "sfg_inspect has not run");
+  return guarded(P, [&] {
+    DeviceScope ds(P->device);
+    LaunchScope ls(P);
+    std::vector<cudaEvent_t> ev((size_t)2 * reps + 2, nullptr);
+    for (auto& e : ev)
+      SFG_CUDA(cudaEventCreate(&e));
+    SFG_CUDA(cudaEventRecord(ev[0], P->stream));
+    for (int r = 0; r < reps; ++r) {
+      if (unfused)
+        exec_unfused_impl(P, ev[(size_t)2 + 2 * r], ev[(size_t)3 + 2 * r]);
+      else
+        exec_fused_impl(P, ev[(size_t)2 + 2 * r], ev[(size_t)3 + 2 * r]);
+    }
+    SFG_CUDA(cudaEventRecord(ev[1], P->stream));
+    SFG_CUDA(cudaEventSynchronize(ev[1]));
+    float tot = 0.f, ksum = 0.f;
+    SFG_CUDA(cudaEventElapsedTime(&tot, ev[0], ev[1]));
+    for (int r = 0; r < reps; ++r) {
+      float ms = 0.f;
+      SFG_CUDA(cudaEventElapsedTime(&ms, ev[(size_t)2 + 2 * r], ev[(size_t)3 + 2 * r]));
+      ksum += ms;
+    }
+    for (auto& e : ev)
+      cudaEventDestroy(e);
+    if (total_ms)
+      *total_ms = tot;
+    if (kernel_ms_avg)
+      *kernel_ms_avg = ksum / (float)reps;
+    return check_error_word(P);
+  });
+}
 
 sfg_status sfg_last_exec_ms(sfg_plan* P, float* total_ms, float* kernel_ms) {
   if (!P || !P->timed)
