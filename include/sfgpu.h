@@ -153,6 +153,13 @@ sfg_status sfg_last_exec_ms(sfg_plan* plan, float* total_ms, float* kernel_ms);
 sfg_status sfg_bench_executions(sfg_plan* plan, int32_t reps, int32_t unfused,
                                 float* total_ms, float* kernel_ms_avg);
 
+/* Device self-test: draws n random (v, d) pairs and counts the pairs where
+ * the executor's division from a precomputed reciprocal differs, bit for
+ * bit, from IEEE __ddiv_rn (expected 0); fast_path counts pairs that took the
+ * reciprocal path. */
+sfg_status sfg_selftest_division(int64_t n, uint64_t seed, int64_t* mismatches,
+                                 int64_t* fast_path);
+
 /* Fixtures (replaces fixtures.hpp generators + the BASELINE configs) -------
  * Generated matrices are returned through an opaque handle. */
 typedef struct sfg_matrix sfg_matrix;

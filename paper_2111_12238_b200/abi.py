@@ -25,7 +25,7 @@ SFG_ERR_NO_DEVICE = 6
 # Every function include/sfgpu.h declares (checked by tests/test_abi.py).
 EXPORTS = (
     "sfg_device_check", "sfg_version", "sfg_set_device", "sfg_host_alloc",
-    "sfg_host_free", "sfg_bench_executions", "sfg_plan_create", "sfg_plan_destroy",
+    "sfg_host_free", "sfg_bench_executions", "sfg_selftest_division", "sfg_plan_create", "sfg_plan_destroy",
     "sfg_plan_set_stream", "sfg_plan_info", "sfg_set_vin", "sfg_inspect",
     "sfg_get_dag", "sfg_get_interdep", "sfg_get_levels", "sfg_compute_reuse",
     "sfg_get_schedule", "sfg_execute_fused", "sfg_execute_unfused",
@@ -71,6 +71,8 @@ def load(path: str | None = None):
     L.sfg_bench_executions.argtypes = [vp, C.c_int32, C.c_int32, C.POINTER(C.c_float),
                                        C.POINTER(C.c_float)]
     L.sfg_bench_executions.restype = st
+    L.sfg_selftest_division.argtypes = [C.c_int64, C.c_uint64, i64p, i64p]
+    L.sfg_selftest_division.restype = st
     L.sfg_plan_create.argtypes = [C.c_int32, C.c_int32, i32p, i32p, f64p, C.c_int32, f64p,
                                   C.c_uint64, C.POINTER(vp)]
     L.sfg_plan_create.restype = st

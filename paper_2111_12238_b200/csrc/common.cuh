@@ -42,11 +42,11 @@ __device__ __forceinline__ void st_relaxed_i32(int* p, int v) {
   asm volatile("st.relaxed.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
-// Spin until *p != SENT; an optional exponential nanosleep backoff (capped at
+// Spin until *p is published (high word not all-ones, see publish_f64); an optional exponential nanosleep backoff (capped at
 // g_sleep_cap ns; 0 = pure spin) keeps pollers off the producers' L2 slices.
 __device__ __forceinline__ double poll_f64(const double* p, unsigned sleep_cap = 160) {
   unsigned long long v = ld_relaxed_u64(p);
-  if (v != SENT)
+  if ((unsigned)(v >> 32) != 0xFFFFFFFFu)
     return __longlong_as_double((long long)v);
   unsigned ns = 20;
   do {
@@ -55,17 +55,22 @@ __device__ __forceinline__ double poll_f64(const double* p, unsigned sleep_cap =
       ns = ns < sleep_cap ? ns * 2 : sleep_cap;
     }
     v = ld_relaxed_u64(p);
-  } while (v == SENT);
+  } while ((unsigned)(v >> 32) == 0xFFFFFFFFu);
   return __longlong_as_double((long long)v);
 }
 
-// Publish a value; a computed all-ones NaN (only possible from SENT-like NaN
-// inputs) is canonicalised so it can never be mistaken for "not ready".
+// Publish a value.  Every NaN is stored as the canonical quiet NaN, so no
+// published word -- and no finite value -- has an all-ones high word: a
+// consumer can test readiness on the high 32 bits alone (is_sent_hi).
 __device__ __forceinline__ void publish_f64(double* p, double v) {
   unsigned long long b = (unsigned long long)__double_as_longlong(v);
-  if (b == SENT)
+  if (v != v)
     b = CANON_NAN;
   st_relaxed_u64(p, b);
+}
+
+__device__ __forceinline__ bool is_sent_hi(unsigned long long w) {
+  return (unsigned)(w >> 32) == 0xFFFFFFFFu;
 }
 
 // Integer flavour for the inspector: 0 = not ready (levels are >= 1).
@@ -116,6 +121,29 @@ __device__ __forceinline__ void report_error(unsigned long long* word,
       ((unsigned long long)(kernel - 1) << 62) |
       ((unsigned long long)(unsigned)seq_pos << 31) | (unsigned)index;
   atomicMin(word, key);
+}
+
+// Correctly rounded v / d given r = RN(1/d) computed earlier (off the
+// critical path): q0 = RN(v r), rho = v - q0 d (exact with FMA), q = RN(q0 +
+// rho r) -- Markstein's correction, which returns RN(v / d) when r is the
+// correctly rounded reciprocal and no intermediate leaves the normal range.
+// Operands near the exponent limits, zeros, infinities and NaNs take the
+// IEEE division itself, so the result always equals __ddiv_rn(v, d)
+// (checked by sfg_selftest_division over random operands).
+static __device__ __noinline__ double ieee_div_slow(double v, double d) { return __ddiv_rn(v, d); }
+
+// biased exponent of |x| inside [2^-500, 2^500): 523 <= e <= 1522
+__device__ __forceinline__ bool exp_in_safe_range(double x) {
+  const unsigned e = (unsigned)((unsigned long long)__double_as_longlong(x) >> 52) & 0x7FFu;
+  return e - 523u < 1000u;
+}
+
+__device__ __forceinline__ double div_with_rcp(double v, double d, double r) {
+  const double q0 = __dmul_rn(v, r);
+  const double q = __fma_rn(__fma_rn(-q0, d, v), r, q0);
+  if (__builtin_expect(!(exp_in_safe_range(v) && exp_in_safe_range(d)), 0))
+    return ieee_div_slow(v, d);
+  return q;
 }
 
 __device__ __forceinline__ double ldg_f64(const double* p) { return __ldg(p); }

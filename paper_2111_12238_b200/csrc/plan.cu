@@ -3,7 +3,7 @@
 // / inter_dag / joint_dag / level_info / compute_reuse / execute_fused /
 // execute_unfused / collect_outputs (kernels.hpp, dag.hpp, executor.hpp).
 #include "../../include/sfgpu.h"
-#include "bsf.cuh"
+#include "chain.cuh"
 #include "common.cuh"
 #include "executor.cuh"
 #include "internal.hpp"
@@ -12,6 +12,7 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <cstdio>
 #include <cstring>
 #include <memory>
 #include <random>
@@ -57,14 +58,15 @@ struct sfg_plan {
   int32_t crit[3] = {0, 0, 0};
   bool have_levels[3] = {false, false, false};
 
-  // blocked sync-free executor (combos 1, 4, 8)
-  bool use_bsf = false;
-  BsfLayout bsf_f, bsf_b;
-  DBuf<int32_t> tick_fused, tick_unfused;
-  int64_t nt = 0, nt_k1 = 0;
-  int32_t y_block = 0, y_blocks = 0;
-  std::vector<int32_t> row_maxcol; // combo 4: last x index each SpMV row reads
-  std::vector<int32_t> host_tickets;
+  // chain executor (combos 1, 4, 8); the level-set kernel stays available
+  // as SFG_EXECUTOR=levels for ablations
+  bool use_chain = false;
+  ChainLayout ch_f, ch_b;
+  DBuf<int32_t> tail_ptr, tail_rows;
+  std::vector<int32_t> row_maxcol; // (unused by the chain path; kept for stats)
+  int32_t tile_rows = 0;           // chain tile height override (S == 1)
+  DBuf<unsigned long long> trace;  // SFG_TRACE diagnostics
+  int32_t trace_tiles = 0;
 
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
   bool timed = false;
@@ -605,79 +607,57 @@ void do_inspect(sfg_plan* P) {
   }
   if (combo == 1 || combo == 4 || combo == 8) {
     const char* ex = getenv("SFG_EXECUTOR");
-    P->use_bsf = ex && std::string(ex) == "bsf";
+    P->use_chain = !(ex && std::string(ex) == "levels");
   }
-  if (P->use_bsf) {
-    const int32_t S = P->nsys;
-    int32_t B = S >= 8 ? 16384 / S : 8192 / S;
-    if (combo == 1)
-      B /= 2;
-    if (const char* e = getenv("SFG_BSF_B"))
-      B = std::max(32, atoi(e));
-    B = std::max<int32_t>(1, std::min<int32_t>(B, std::max<int32_t>(n, 1)));
-    const int32_t bmax = (200 * 1024) / (8 * S * (combo == 1 ? 2 : 1));
-    B = std::min(B, bmax);
-    build_bsf(P->lr_ptr.p, P->lr_idx.p, P->lr_val.p, n, S, +1, B, P->bsf_f, s);
+  if (P->use_chain) {
+    if (const char* e = getenv("SFG_CHAIN_G"))
+      P->tile_rows = atoi(e);
+    const int32_t G = chain_G(P->nsys, P->tile_rows), CS = chain_CS(P->nsys);
+    int32_t max_len = 4096;
+    if (const char* e = getenv("SFG_CHAIN_MAX"))
+      max_len = atoi(e);
+    build_chains(P->lr_ptr.p, P->lr_idx.p, n, +1, G, CS, max_len, P->ch_f, s);
     if (combo == 8)
-      build_bsf(P->lt_ptr.p, P->lt_idx.p, P->lt_val.p, n, S, -1, B, P->bsf_b, s);
-    std::vector<int32_t> y_after;
-    if (combo == 4) {
-      P->y_block = std::max<int32_t>(256, B / 2);
-      P->y_blocks = (n + P->y_block - 1) / P->y_block;
-      y_after.assign((size_t)P->y_blocks, -1);
-      for (int32_t r = 0; r < n; ++r) {
-        const int32_t j = P->row_maxcol[(size_t)r];
-        const int32_t k = r / P->y_block;
-        if (j >= 0)
-          y_after[(size_t)k] = std::max(y_after[(size_t)k], j / B);
-      }
+      build_chains(P->lt_ptr.p, P->lt_idx.p, n, -1, G, CS, max_len, P->ch_b, s);
+    if (combo == 4)
+      build_tails(P->ch_f, P->ar_ptr.p, P->ar_idx.p, n, P->tail_ptr, P->tail_rows, s);
+    if (getenv("SFG_TRACE")) {
+      P->trace_tiles = getenv("SFG_TRACE_TILES") ? atoi(getenv("SFG_TRACE_TILES")) : 160;
+      const int64_t items = (int64_t)P->ch_f.nbatch + P->ch_b.nbatch;
+      P->trace.alloc(items * P->trace_tiles * 3);
+      SFG_CUDA(cudaMemsetAsync(P->trace.p, 0, sizeof(unsigned long long) * items * P->trace_tiles * 3, s));
     }
-    P->host_tickets = bsf_tickets(combo, P->bsf_f, combo == 8 ? &P->bsf_b : nullptr, P->y_blocks,
-                                  y_after, &P->nt_k1);
-    P->nt = (int64_t)P->host_tickets.size();
-    upload(P->tick_fused, P->host_tickets.data(), P->nt, s);
-    std::vector<int32_t> unf;
-    for (int32_t b = 0; b < P->bsf_f.nblk; ++b)
-      unf.push_back(ticket(TK_FWD, b));
-    for (int32_t b = 0; b < P->bsf_b.nblk; ++b)
-      unf.push_back(ticket(TK_BWD, b));
-    for (int32_t k = 0; k < P->y_blocks; ++k)
-      unf.push_back(ticket(TK_Y, k));
-    upload(P->tick_unfused, unf.data(), (int64_t)unf.size(), s);
-    SFG_CUDA(cudaStreamSynchronize(s));
-    // the blocked layouts carry their own copies of the values
-    P->lr_val.release();
-    P->lt_val.release();
   }
   SFG_CUDA(cudaStreamSynchronize(s));
   P->inspected = true;
 }
 
-BsfArgs bsf_args(sfg_plan* P) {
-  BsfArgs a;
+ChainArgs chain_args(sfg_plan* P) {
+  ChainArgs a;
   a.combo = P->combo;
   a.n = P->n;
   a.S = P->nsys;
   a.counter = P->counter.p;
   a.err = P->err.p;
-  a.Bf = P->bsf_f.B;
-  a.nblk_f = P->bsf_f.nblk;
-  a.f_rowP = P->bsf_f.rowP.p;
-  a.f_ptr = P->bsf_f.nptr.p;
-  a.f_idx = P->bsf_f.nidx.p;
-  a.f_val = P->bsf_f.nval.p;
-  a.f_diag = P->bsf_f.dval.p;
-  a.f_bptr = P->bsf_f.bptr.p;
-  a.f_blkb = P->bsf_f.blk_batch.p;
-  a.Bb = P->bsf_b.B;
-  a.b_rowP = P->bsf_b.rowP.p;
-  a.b_ptr = P->bsf_b.nptr.p;
-  a.b_idx = P->bsf_b.nidx.p;
-  a.b_val = P->bsf_b.nval.p;
-  a.b_diag = P->bsf_b.dval.p;
-  a.b_bptr = P->bsf_b.bptr.p;
-  a.b_blkb = P->bsf_b.blk_batch.p;
-  a.By = P->y_block;
+  a.lr_ptr = P->lr_ptr.p;
+  a.lr_idx = P->lr_idx.p;
+  a.lr_val = P->lr_val.p;
+  a.f_cstart = P->ch_f.cstart.p;
+  a.f_corder = P->ch_f.corder.p;
+  a.f_bptr = P->ch_f.batch_ptr.p;
+  a.f_level = P->ch_f.clevel.p;
+  a.f_nbatch = P->ch_f.nbatch;
+  a.lt_ptr = P->lt_ptr.p;
+  a.lt_idx = P->lt_idx.p;
+  a.lt_val = P->lt_val.p;
+  a.b_cstart = P->ch_b.cstart.p;
+  a.b_corder = P->ch_b.corder.p;
+  a.b_bptr = P->ch_b.batch_ptr.p;
+  a.b_level = P->ch_b.clevel.p;
+  a.b_nbatch = P->ch_b.nbatch;
+  a.tail_ptr = P->tail_ptr.p;
+  a.tile_rows = P->tile_rows;
+  a.tail_rows = P->tail_rows.p;
   a.ar_ptr = P->ar_ptr.p;
   a.ar_idx = P->ar_idx.p;
   a.ar_val = P->ar_val.p;
@@ -686,6 +666,10 @@ BsfArgs bsf_args(sfg_plan* P) {
   a.vout = P->vout.p;
   if (const char* e = getenv("SFG_BLOCKS_PER_SM"))
     a.blocks_per_sm = atoi(e);
+  if (P->trace.p) {
+    a.trace = P->trace.p;
+    a.trace_tiles = P->trace_tiles;
+  }
   return a;
 }
 
@@ -930,12 +914,12 @@ void exec_fused_impl(sfg_plan* P, cudaEvent_t kb, cudaEvent_t ke) {
   }
   launch_prep(r, nr, P->counter.p, P->err.p, P->stream);
   SFG_CUDA(cudaEventRecord(kb, P->stream));
-  if (P->use_bsf) {
-    BsfArgs b = bsf_args(P);
+  if (P->use_chain) {
+    ChainArgs b = chain_args(P);
     b.phase = 3;
-    b.tickets = P->tick_fused.p;
-    b.nt = P->nt;
-    launch_bsf(b, P->stream);
+    b.seg_begin = 0;
+    b.seg_end = P->ch_f.nbatch + (P->combo == 8 ? P->ch_b.nbatch : 0);
+    launch_chain(b, P->stream);
   } else {
     ExecArgs a = exec_args(P);
     a.phase = 3;
@@ -961,25 +945,23 @@ void exec_unfused_impl(sfg_plan* P, cudaEvent_t kb, cudaEvent_t ke) {
     r1[n1++] = {P->fac.p, P->nnzF};
   launch_prep(r1, n1, P->counter.p, P->err.p, P->stream);
   SFG_CUDA(cudaEventRecord(kb, P->stream));
-  if (P->use_bsf) {
-    BsfArgs b = bsf_args(P);
+  if (P->use_chain) {
+    ChainArgs b = chain_args(P);
     b.phase = 1;
-    b.tickets = P->tick_unfused.p;
-    b.nt = P->nt_k1;
-    launch_bsf(b, P->stream);
+    b.seg_begin = 0;
+    b.seg_end = P->ch_f.nbatch;
+    launch_chain(b, P->stream);
     FillRegion r2[1];
     int n2 = 0;
     if (c == 1 || c == 8)
       r2[n2++] = {P->vout.p, nv};
     launch_prep(r2, n2, P->counter.p, nullptr, P->stream);
     b.phase = 2;
-    if (c == 1) {
-      b.nt = P->nt_k1;
-    } else {
-      b.tickets = P->tick_unfused.p + P->nt_k1;
-      b.nt = P->nt - P->nt_k1;
+    if (c == 8) {
+      b.seg_begin = P->ch_f.nbatch;
+      b.seg_end = P->ch_f.nbatch + P->ch_b.nbatch;
     }
-    launch_bsf(b, P->stream);
+    launch_chain(b, P->stream);
     SFG_CUDA(cudaEventRecord(ke, P->stream));
     return;
   }
@@ -1110,6 +1092,18 @@ sfg_status sfg_plan_destroy(sfg_plan* P) {
     DeviceScope ds(P->device);
     if (P->stream)
       cudaStreamSynchronize(P->stream);
+    if (P->trace.p) {
+      // SFG_TRACE=<path>: binary dump {items, tiles, data[items*tiles*3]}
+      const int64_t items = (int64_t)P->ch_f.nbatch + P->ch_b.nbatch;
+      std::vector<unsigned long long> h((size_t)(items * P->trace_tiles * 3));
+      cudaMemcpy(h.data(), P->trace.p, sizeof(unsigned long long) * h.size(), cudaMemcpyDeviceToHost);
+      if (FILE* f = fopen(getenv("SFG_TRACE"), "wb")) {
+        const int64_t hdr[3] = {items, P->trace_tiles, P->ch_f.nbatch};
+        fwrite(hdr, sizeof(hdr), 1, f);
+        fwrite(h.data(), sizeof(unsigned long long), h.size(), f);
+        fclose(f);
+      }
+    }
     for (auto& e : P->ev)
       if (e)
         cudaEventDestroy(e);
@@ -1288,48 +1282,59 @@ sfg_status sfg_get_schedule(sfg_plan* P, int64_t* nentries, uint8_t* tags, int32
     return SFG_ERR_INVALID_ARGUMENT;
   if (!P->inspected)
     return set_err(P, SFG_ERR_LOGIC, "sfg_inspect has not run");
-  if (P->use_bsf) {
+  if (P->use_chain) {
     return guarded(P, [&] {
       DeviceScope ds(P->device);
       const int32_t n = P->n;
-      std::vector<int32_t> rf((size_t)n), rb;
-      if (n)
-        SFG_CUDA(cudaMemcpy(rf.data(), P->bsf_f.rowP.p, sizeof(int32_t) * (size_t)n,
-                            cudaMemcpyDeviceToHost));
-      if (P->combo == 8) {
-        rb.resize((size_t)n);
-        if (n)
-          SFG_CUDA(cudaMemcpy(rb.data(), P->bsf_b.rowP.p, sizeof(int32_t) * (size_t)n,
-                              cudaMemcpyDeviceToHost));
-      }
+      auto fetch = [](const DBuf<int32_t>& d, int64_t cnt) {
+        std::vector<int32_t> h((size_t)std::max<int64_t>(cnt, 0));
+        if (cnt > 0)
+          SFG_CUDA(cudaMemcpy(h.data(), d.p, sizeof(int32_t) * (size_t)cnt, cudaMemcpyDeviceToHost));
+        return h;
+      };
       std::vector<uint8_t> tg;
       std::vector<int32_t> it;
       std::vector<int64_t> wp{0};
-      for (int32_t tk : P->host_tickets) {
-        const int kind = tk >> 28, bi = tk & 0x0FFFFFFF;
-        if (kind == TK_Y) {
-          for (int32_t r = bi * P->y_block; r < std::min(n, (bi + 1) * P->y_block); ++r) {
-            tg.push_back(2);
-            it.push_back(r);
-          }
-        } else {
-          const BsfLayout& L = kind == TK_BWD ? P->bsf_b : P->bsf_f;
-          for (int32_t q = bi * L.B; q < std::min(n, (bi + 1) * L.B); ++q) {
-            if (kind == TK_BWD) {
-              tg.push_back(2);
-              it.push_back(n - 1 - rb[(size_t)q]);
-            } else {
-              tg.push_back(1);
-              it.push_back(rf[(size_t)q]);
-              if (P->combo == 1) {
+      auto emit = [&](const ChainLayout& L, bool bwd) {
+        const auto cs = fetch(L.cstart, (int64_t)L.nchain + 1);
+        const auto co = fetch(L.corder, L.nchain);
+        const auto bp = fetch(L.batch_ptr, (int64_t)L.nbatch + 1);
+        std::vector<int32_t> tp, tr;
+        if (P->combo == 4 && !bwd) {
+          tp = fetch(P->tail_ptr, (int64_t)L.nchain + 1);
+          tr = fetch(P->tail_rows, n);
+        }
+        for (int32_t bi = 0; bi < L.nbatch; ++bi) {
+          for (int32_t q = bp[(size_t)bi]; q < bp[(size_t)bi + 1]; ++q) {
+            const int32_t c = co[(size_t)q];
+            for (int32_t p = cs[(size_t)c]; p < cs[(size_t)c + 1]; ++p) {
+              if (bwd) {
                 tg.push_back(2);
-                it.push_back(rf[(size_t)q]);
+                it.push_back(p); // reversed numbering i' = n-1-row = position
+              } else {
+                tg.push_back(1);
+                it.push_back(p);
+                if (P->combo == 1) {
+                  tg.push_back(2);
+                  it.push_back(p);
+                }
               }
             }
           }
+          if (!tp.empty())
+            for (int32_t q = bp[(size_t)bi]; q < bp[(size_t)bi + 1]; ++q) {
+              const int32_t c = co[(size_t)q];
+              for (int32_t t = tp[(size_t)c]; t < tp[(size_t)c + 1]; ++t) {
+                tg.push_back(2);
+                it.push_back(tr[(size_t)t]);
+              }
+            }
+          wp.push_back((int64_t)tg.size());
         }
-        wp.push_back((int64_t)tg.size());
-      }
+      };
+      emit(P->ch_f, false);
+      if (P->combo == 8)
+        emit(P->ch_b, true);
       if (nentries)
         *nentries = (int64_t)tg.size();
       if (nwaves)

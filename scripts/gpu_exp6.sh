@@ -1,0 +1,10 @@
+mkdir -p gpurun_out
+run() {
+  envs="$1"; shift
+  timeout 300 env $envs python bench.py --steps 10 --warmup 3 --no-cpu-baseline --no-extras "$@" > /tmp/o.json 2>/tmp/e.txt
+  python -c "import json,sys;d=json.load(open('/tmp/o.json'));print('$envs $* ms=%.3f kernel=%.3f unfused=%.3f frac=%.3f e2e=%.2f'%(d['ms_per_step'],d['roofline']['kernel_ms'],d['unfused']['ms_per_step'],d['roofline']['frac'],d['e2e']['ms_per_step']))" >> gpurun_out/exp6.txt 2>&1 || (echo "$envs $* FAILED" >> gpurun_out/exp6.txt; tail -3 /tmp/e.txt >> gpurun_out/exp6.txt)
+}
+for g in 1 2 4 8; do run "SFG_CHAIN_G=$g" --config 1; done
+run "SFG_BLOCKS_PER_SM=1" --config 5
+run "SFG_X=1" --config 5 --systems-per-gpu 4
+run "SFG_X=1" --config 5 --systems-per-gpu 16

@@ -235,3 +235,16 @@ def test_config1_residuals():
     L = sp.tril(A).tocsr()
     assert np.max(np.abs(L @ z - b)) <= 1e-12 * np.max(np.abs(b))
     assert np.max(np.abs(A @ z - y)) <= 1e-12 * max(1, np.max(np.abs(y)))
+
+
+def test_division_from_reciprocal_is_ieee():
+    # the executors divide with a reciprocal staged off the critical path;
+    # it must equal IEEE division bit for bit
+    import ctypes as C
+    from paper_2111_12238_b200 import abi
+    bad = C.c_int64(-1)
+    fast = C.c_int64(0)
+    n = 1 << 28
+    assert abi.load().sfg_selftest_division(n, 12345, C.byref(bad), C.byref(fast)) == 0
+    assert bad.value == 0
+    assert fast.value > n // 10
