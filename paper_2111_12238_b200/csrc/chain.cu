@@ -524,11 +524,277 @@ __global__ void __launch_bounds__(kThreads) k_chain(const ChainArgs A) {
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// Shared-memory-staged variant for S >= 2 systems (the batched solves).
+// Stage C copies the next tile's values and first x reads into a per-warp
+// double buffer with cp.async.cg (16-byte, L2-coherent: the pair of systems
+// s, s+1 of one nonzero / one x row is contiguous), so the staged data holds
+// no registers while in flight and twice as many warps fit on an SM.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void cp_async_cg16(void* smem, const void* gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() {
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void cp_async_wait1() {
+  asm volatile("cp.async.wait_group 1;" ::: "memory");
+}
+
+template <int S, int G, int CHN> struct StageBuf {
+  double v[G][CHN][S];
+  unsigned long long x[G][CHN][S];
+};
+
+template <int S, int G, int CHN, int COMBO>
+__global__ void __launch_bounds__(kThreads, 2) k_chain_sm(const ChainArgs A) {
+  static_assert(S >= 2 && S % 2 == 0, "pair copies need an even number of systems");
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  StageBuf<S, G, CHN>* wbuf =
+      reinterpret_cast<StageBuf<S, G, CHN>*>(smem_raw) + 2 * (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  const int k = lane / S;
+  const int s = lane % S;
+  const bool lane_on = k < G;
+  const bool copier = (s & 1) == 0;
+  const int total = A.seg_end - A.seg_begin;
+  for (;;) {
+    unsigned long long w0 = 0;
+    if (lane == 0)
+      w0 = atomicAdd(A.counter, 1ull);
+    const long long wi = (long long)__shfl_sync(FULL, w0, 0);
+    if (wi >= total)
+      break;
+    const int item = A.seg_begin + (int)wi;
+    const bool bwd = item >= A.f_nbatch;
+    const int bi = bwd ? item - A.f_nbatch : item;
+    const int32_t* ptr = bwd ? A.lt_ptr : A.lr_ptr;
+    const int32_t* idx = bwd ? A.lt_idx : A.lr_idx;
+    const double* val = bwd ? A.lt_val : A.lr_val;
+    const int32_t* cstart = bwd ? A.b_cstart : A.f_cstart;
+    const int32_t* corder = bwd ? A.b_corder : A.f_corder;
+    const int32_t* bptr = bwd ? A.b_bptr : A.f_bptr;
+    const int32_t* clev = bwd ? A.b_level : A.f_level;
+    const int c = __ldg(corder + __ldg(bptr + bi));
+    const int p0 = __ldg(cstart + c);
+    const int len = __ldg(cstart + c + 1) - p0;
+    const int skew = __ldg(clev + c) % G;
+    const int ntiles = (len + skew + G - 1) / G;
+    double* xo = bwd ? A.vout : A.vmid;
+    const double* rhs_vec = bwd ? A.vmid : A.vin;
+    const int kern = bwd ? 2 : 1;
+    const bool pass1 = COMBO != 1 || (A.phase & 1);
+    const bool pass2 = COMBO == 1 && (A.phase & 2);
+    const double* xs = pass1 ? xo : A.vout;
+    const double* rs = pass1 ? rhs_vec : A.vmid;
+    const bool rpoll = pass1 ? bwd : true;
+    unsigned long long* tr = A.trace ? A.trace + (size_t)item * A.trace_tiles * 3 : nullptr;
+    const unsigned long long t_claim = tr ? gtimer() : 0ull;
+    auto row_of = [&](int o) { const int p = p0 + o; return bwd ? A.n - 1 - p : p; };
+    auto active = [&](int tile) {
+      const int o = G * tile - skew + k;
+      return lane_on && tile >= 0 && tile < ntiles && o >= 0 && o < len;
+    };
+    int pb3 = 0, pe3 = 0;
+    int b2 = 0, eend2 = 0, e2 = 0;
+    bool act2 = false;
+    int idx2[CHN];
+    // current tile (scalars in registers, values / x words in smem)
+    int cr = 0, cb = 0, ceend = 0;
+    bool cact = false, cchained = false;
+    int cjj[CHN];
+    double cd = 1.0, cvc = 0.0, crd = 1.0;
+    unsigned long long crhs = 0;
+    double carry = 0.0, carry2 = 0.0;
+    __syncwarp();
+#pragma unroll 1
+    for (int t = -3; t < ntiles; ++t) {
+      // stage A: row pointers of tile t+3
+      int npb = 0, npe = 0;
+      if (active(t + 3)) {
+        const int r = row_of(G * (t + 3) - skew + k);
+        npb = __ldg(ptr + r);
+        npe = __ldg(ptr + r + 1);
+      }
+      // stage B: dependency indices of tile t+2
+      const bool nact2 = active(t + 2);
+      int nb2 = 0, ne2 = 0, neend2 = 0;
+      int nidx2[CHN];
+      if (nact2) {
+        nb2 = pb3;
+        ne2 = pe3 - 1;
+        neend2 = (G * (t + 2) - skew + k) > 0 ? ne2 - 1 : ne2;
+        const int32_t* ib = idx + nb2;
+        const int m = neend2 - nb2;
+#pragma unroll
+        for (int a = 0; a < CHN; ++a)
+          if (a < m)
+            nidx2[a] = __ldg(ib + a);
+      }
+      // stage C: tile t+1 -> smem buffer (t+1)&1 by 16-byte async copies
+      StageBuf<S, G, CHN>& nb = wbuf[(t + 1) & 1];
+      int nr = 0;
+      bool nchained = false;
+      double nd = 1.0, nvc = 0.0;
+      unsigned long long nrhs = 0;
+      if (act2) {
+        const int o = G * (t + 1) - skew + k;
+        nchained = o > 0;
+        nr = row_of(o);
+        nd = __ldg(val + (size_t)e2 * S + s);
+        nvc = nchained ? __ldg(val + (size_t)(e2 - 1) * S + s) : 0.0;
+        nrhs = rpoll ? ld_relaxed_u64(rs + (size_t)nr * S + s)
+                     : (unsigned long long)__double_as_longlong(__ldg(rs + (size_t)nr * S + s));
+        if (copier) {
+          const int m = eend2 - b2;
+          const double* vb = val + (size_t)b2 * S + s;
+          const double* xb = xs + s;
+#pragma unroll
+          for (int a = 0; a < CHN; ++a)
+            if (a < m) {
+              cp_async_cg16(&nb.v[k][a][s], vb + a * S);
+              cp_async_cg16(&nb.x[k][a][s], xb + (size_t)idx2[a] * S);
+            }
+        }
+      }
+      cp_async_commit();
+      // stage D: complete tile t from smem buffer t&1
+      if (t >= 0) {
+        const long long c0 = tr ? clock64() : 0;
+        cp_async_wait1();
+        __syncwarp();
+        const unsigned long long t_part = tr ? gtimer() : 0ull;
+        long long c1 = 0;
+        const StageBuf<S, G, CHN>& cbuf = wbuf[t & 1];
+        const int r = cr;
+        double x = 0.0;
+        if (pass1) {
+          double acc = 0.0;
+          if (cact) {
+            acc = crhs != SENT ? __longlong_as_double((long long)crhs)
+                               : poll_f64(rhs_vec + (size_t)r * S + s, 0);
+            const int m = ceend - cb < CHN ? ceend - cb : CHN;
+            unsigned long long xx[CHN];
+#pragma unroll
+            for (int a = 0; a < CHN; ++a)
+              if (a < m)
+                xx[a] = cbuf.x[k][a][s];
+            for (;;) {
+              bool pending = false;
+#pragma unroll
+              for (int a = 0; a < CHN; ++a)
+                pending |= a < m && is_sent_hi(xx[a]);
+              if (!pending)
+                break;
+#pragma unroll
+              for (int a = 0; a < CHN; ++a)
+                if (a < m && is_sent_hi(xx[a]))
+                  xx[a] = ld_relaxed_u64(xo + (size_t)cjj[a] * S + s);
+            }
+#pragma unroll
+            for (int a = 0; a < CHN; ++a)
+              if (a < m)
+                acc = __dsub_rn(acc, __dmul_rn(cbuf.v[k][a][s],
+                                               __longlong_as_double((long long)xx[a])));
+            for (int p = cb + CHN; p < ceend; ++p) // rows longer than the staging width
+              acc = __dsub_rn(acc, __dmul_rn(__ldg(val + (size_t)p * S + s),
+                                             poll_f64(xo + (size_t)__ldg(idx + p) * S + s, 0)));
+            if (cd == 0.0)
+              report_error(A.err, kern, bwd ? A.n - 1 - r : r, r);
+          }
+          if (tr)
+            c1 = clock64();
+#pragma unroll
+          for (int kk = 0; kk < G; ++kk) {
+            const double v = cchained ? __dsub_rn(acc, __dmul_rn(cvc, carry)) : acc;
+            const double q0 = __dmul_rn(v, crd);
+            double q = __fma_rn(__fma_rn(-q0, cd, v), crd, q0);
+            const bool mine = cact && k == kk;
+            if (__builtin_expect(mine && !(exp_in_safe_range(v) && exp_in_safe_range(cd)), 0))
+              q = ieee_div_slow(v, cd);
+            if (mine) {
+              x = q;
+              publish_f64(xo + (size_t)r * S + s, q);
+            }
+            carry = __shfl_sync(FULL, x, kk * S + s);
+          }
+        }
+        if (pass2) { // combo 1: x2 = inv(L) z on the same rows
+          double acc2 = 0.0;
+          if (cact) {
+            const double z = pass1 ? x
+                                   : (crhs != SENT ? __longlong_as_double((long long)crhs)
+                                                   : poll_f64(A.vmid + (size_t)r * S + s, 0));
+            acc2 = partial_sum<S>(z, cb, ceend, idx, val, A.vout, s);
+            if (cd == 0.0)
+              report_error(A.err, 2, r, r);
+          }
+          double x2 = 0.0;
+#pragma unroll
+          for (int kk = 0; kk < G; ++kk) {
+            const double v = cchained ? __dsub_rn(acc2, __dmul_rn(cvc, carry2)) : acc2;
+            const double q0 = __dmul_rn(v, crd);
+            double q = __fma_rn(__fma_rn(-q0, cd, v), crd, q0);
+            const bool mine = cact && k == kk;
+            if (__builtin_expect(mine && !(exp_in_safe_range(v) && exp_in_safe_range(cd)), 0))
+              q = ieee_div_slow(v, cd);
+            if (mine) {
+              x2 = q;
+              publish_f64(A.vout + (size_t)r * S + s, q);
+            }
+            carry2 = __shfl_sync(FULL, x2, kk * S + s);
+          }
+        }
+        if (tr && lane == 0 && t < A.trace_tiles) {
+          // {claim (globaltimer ns), wait-phase cycles << 32 | carry cycles,
+          //  tile end (globaltimer ns)}
+          const long long c2 = clock64();
+          tr[t * 3 + 0] = t_claim;
+          tr[t * 3 + 1] = ((unsigned long long)(c1 - c0) << 32) | (unsigned long long)(c2 - c1);
+          tr[t * 3 + 2] = gtimer();
+          (void)t_part;
+        }
+      }
+      // rotate
+      cr = nr;
+      cb = b2;
+      ceend = eend2;
+      cact = act2;
+      cchained = nchained;
+      cd = nd;
+      cvc = nvc;
+      crd = act2 ? __drcp_rn(nd) : 1.0;
+      crhs = nrhs;
+#pragma unroll
+      for (int a = 0; a < CHN; ++a)
+        cjj[a] = idx2[a];
+      act2 = nact2;
+      b2 = nb2;
+      e2 = ne2;
+      eend2 = neend2;
+#pragma unroll
+      for (int a = 0; a < CHN; ++a)
+        idx2[a] = nidx2[a];
+      pb3 = npb;
+      pe3 = npe;
+    }
+    // drain this warp's async copies before its buffers are reused
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    __syncwarp();
+  }
+}
+
 template <int S, int G, int COMBO> void launch_g(const ChainArgs& a, cudaStream_t s) {
   constexpr int CHN = 12;
-  auto kern = k_chain<S, G, CHN, COMBO>;
+  constexpr bool use_sm = S >= 2 && S % 2 == 0 && COMBO != 4;
+  auto kern = use_sm ? k_chain_sm<(S >= 2 ? S : 2), G, CHN, COMBO> : k_chain<S, G, CHN, COMBO>;
+  const size_t smem = use_sm ? (size_t)(kThreads / 32) * 2 * sizeof(StageBuf<(S >= 2 ? S : 2), G, CHN>) : 0;
+  if (smem > 48 * 1024)
+    SFG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int per_sm = 0;
-  SFG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, 0));
+  SFG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, smem));
   if (per_sm < 1)
     per_sm = 1;
   if (a.blocks_per_sm > 0 && a.blocks_per_sm < per_sm)
@@ -539,7 +805,7 @@ template <int S, int G, int COMBO> void launch_g(const ChainArgs& a, cudaStream_
     grid = (int64_t)per_sm * sm_count();
   if (grid < 1)
     return;
-  kern<<<(unsigned)grid, kThreads, 0, s>>>(a);
+  kern<<<(unsigned)grid, kThreads, smem, s>>>(a);
   count_launch();
   SFG_CUDA(cudaGetLastError());
 }

@@ -86,7 +86,8 @@ struct ChainArgs {
 // Tile geometry for S interleaved systems: G rows in flight per chain (one
 // chain per warp).
 inline int32_t chain_G(int32_t S, int32_t override_rows = 0) {
-  return S == 1 && override_rows > 0 ? override_rows : (32 / S < 8 ? 32 / S : 8);
+  const int32_t g = 32 / S < 8 ? 32 / S : 8;
+  return (S == 1 || S == 8) && override_rows > 0 && override_rows <= g ? override_rows : g;
 }
 inline int32_t chain_CS(int32_t) { return 1; }
 

@@ -28,6 +28,14 @@ __device__ __forceinline__ unsigned long long ld_relaxed_u64(const void* p) {
   return v;
 }
 
+// Read-only (non-coherent) load pinned in program order (asm volatile), so
+// the compiler cannot hoist it across the executor's wait loops.
+__device__ __forceinline__ double ld_nc_f64(const double* p) {
+  double v;
+  asm volatile("ld.global.nc.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  return v;
+}
+
 __device__ __forceinline__ void st_relaxed_u64(void* p, unsigned long long v) {
   asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }

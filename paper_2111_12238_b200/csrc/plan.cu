@@ -4,6 +4,7 @@
 // execute_unfused / collect_outputs (kernels.hpp, dag.hpp, executor.hpp).
 #include "../../include/sfgpu.h"
 #include "chain.cuh"
+#include "ell.cuh"
 #include "common.cuh"
 #include "executor.cuh"
 #include "internal.hpp"
@@ -62,6 +63,9 @@ struct sfg_plan {
   // as SFG_EXECUTOR=levels for ablations
   bool use_chain = false;
   ChainLayout ch_f, ch_b;
+  bool use_ell = false; // TMA-staged chain-ELL executor (batched combo 8)
+  EllLayout ell_f, ell_b;
+  int32_t ell_chn = 0;
   DBuf<int32_t> tail_ptr, tail_rows;
   std::vector<int32_t> row_maxcol; // (unused by the chain path; kept for stats)
   int32_t tile_rows = 0;           // chain tile height override (S == 1)
@@ -490,9 +494,13 @@ void build_plan(sfg_plan* P, const int32_t* colptr, const int32_t* rowidx,
                                cudaMemcpyHostToDevice, s));
       interleave(P->staging.p, n, S, P->vin.p, s);
     }
-    P->vout.alloc(nv > 0 ? nv : 1);
-    if (combo == 1 || combo == 4 || combo == 8)
-      P->vmid.alloc(nv > 0 ? nv : 1);
+    // one extra all-zero row n: the chain-ELL padding reads it
+    P->vout.alloc(nv + S);
+    SFG_CUDA(cudaMemsetAsync(P->vout.p + nv, 0, sizeof(double) * (size_t)S, s));
+    if (combo == 1 || combo == 4 || combo == 8) {
+      P->vmid.alloc(nv + S);
+      SFG_CUDA(cudaMemsetAsync(P->vmid.p + nv, 0, sizeof(double) * (size_t)S, s));
+    }
   }
   P->counter.alloc(1);
   P->err.alloc(1);
@@ -621,15 +629,59 @@ void do_inspect(sfg_plan* P) {
       build_chains(P->lt_ptr.p, P->lt_idx.p, n, -1, G, CS, max_len, P->ch_b, s);
     if (combo == 4)
       build_tails(P->ch_f, P->ar_ptr.p, P->ar_idx.p, n, P->tail_ptr, P->tail_rows, s);
+    const char* ell_env = getenv("SFG_ELL");
+    if (combo == 8 && P->nsys >= 2 && ell_env && std::string(ell_env) == "1") {
+      const int32_t w = std::max(ell_width(P->lr_ptr.p, P->lr_idx.p, n, +1, P->ch_f, s),
+                                 ell_width(P->lt_ptr.p, P->lt_idx.p, n, -1, P->ch_b, s));
+      const int32_t chn = std::max(4, (w + 3) / 4 * 4);
+      if (chn <= kEllMaxWidth) {
+        P->ell_chn = chn;
+        build_ell(P->lr_ptr.p, P->lr_idx.p, P->lr_val.p, n, P->nsys, +1, chn, P->ch_f, P->ell_f, s);
+        build_ell(P->lt_ptr.p, P->lt_idx.p, P->lt_val.p, n, P->nsys, -1, chn, P->ch_b, P->ell_b, s);
+        P->use_ell = true;
+      }
+    }
     if (getenv("SFG_TRACE")) {
       P->trace_tiles = getenv("SFG_TRACE_TILES") ? atoi(getenv("SFG_TRACE_TILES")) : 160;
       const int64_t items = (int64_t)P->ch_f.nbatch + P->ch_b.nbatch;
       P->trace.alloc(items * P->trace_tiles * 3);
       SFG_CUDA(cudaMemsetAsync(P->trace.p, 0, sizeof(unsigned long long) * items * P->trace_tiles * 3, s));
+      // (the chain-ELL kernel uses one word per tile: the first third)
     }
   }
   SFG_CUDA(cudaStreamSynchronize(s));
   P->inspected = true;
+}
+
+EllArgs ell_args(sfg_plan* P) {
+  EllArgs a;
+  a.n = P->n;
+  a.S = P->nsys;
+  a.counter = P->counter.p;
+  a.err = P->err.p;
+  a.f_cstart = P->ch_f.cstart.p;
+  a.f_corder = P->ch_f.corder.p;
+  a.f_bptr = P->ch_f.batch_ptr.p;
+  a.f_level = P->ch_f.clevel.p;
+  a.f_nbatch = P->ch_f.nbatch;
+  a.f_eidx = P->ell_f.eidx.p;
+  a.f_eval = P->ell_f.eval.p;
+  a.b_cstart = P->ch_b.cstart.p;
+  a.b_corder = P->ch_b.corder.p;
+  a.b_bptr = P->ch_b.batch_ptr.p;
+  a.b_level = P->ch_b.clevel.p;
+  a.b_eidx = P->ell_b.eidx.p;
+  a.b_eval = P->ell_b.eval.p;
+  if (P->trace.p) {
+    a.trace = P->trace.p;
+    a.trace_tiles = P->trace_tiles;
+  }
+  a.vin = P->vin.p;
+  a.vmid = P->vmid.p;
+  a.vout = P->vout.p;
+  if (const char* e = getenv("SFG_BLOCKS_PER_SM"))
+    a.blocks_per_sm = atoi(e);
+  return a;
 }
 
 ChainArgs chain_args(sfg_plan* P) {
@@ -914,7 +966,12 @@ void exec_fused_impl(sfg_plan* P, cudaEvent_t kb, cudaEvent_t ke) {
   }
   launch_prep(r, nr, P->counter.p, P->err.p, P->stream);
   SFG_CUDA(cudaEventRecord(kb, P->stream));
-  if (P->use_chain) {
+  if (P->use_ell) {
+    EllArgs e = ell_args(P);
+    e.seg_begin = 0;
+    e.seg_end = P->ch_f.nbatch + P->ch_b.nbatch;
+    launch_chain_ell(e, P->ell_chn, P->stream);
+  } else if (P->use_chain) {
     ChainArgs b = chain_args(P);
     b.phase = 3;
     b.seg_begin = 0;
@@ -945,6 +1002,19 @@ void exec_unfused_impl(sfg_plan* P, cudaEvent_t kb, cudaEvent_t ke) {
     r1[n1++] = {P->fac.p, P->nnzF};
   launch_prep(r1, n1, P->counter.p, P->err.p, P->stream);
   SFG_CUDA(cudaEventRecord(kb, P->stream));
+  if (P->use_ell) {
+    EllArgs e = ell_args(P);
+    e.seg_begin = 0;
+    e.seg_end = P->ch_f.nbatch;
+    launch_chain_ell(e, P->ell_chn, P->stream);
+    FillRegion r2[1] = {{P->vout.p, nv}};
+    launch_prep(r2, 1, P->counter.p, nullptr, P->stream);
+    e.seg_begin = P->ch_f.nbatch;
+    e.seg_end = P->ch_f.nbatch + P->ch_b.nbatch;
+    launch_chain_ell(e, P->ell_chn, P->stream);
+    SFG_CUDA(cudaEventRecord(ke, P->stream));
+    return;
+  }
   if (P->use_chain) {
     ChainArgs b = chain_args(P);
     b.phase = 1;
@@ -1097,10 +1167,24 @@ sfg_status sfg_plan_destroy(sfg_plan* P) {
       const int64_t items = (int64_t)P->ch_f.nbatch + P->ch_b.nbatch;
       std::vector<unsigned long long> h((size_t)(items * P->trace_tiles * 3));
       cudaMemcpy(h.data(), P->trace.p, sizeof(unsigned long long) * h.size(), cudaMemcpyDeviceToHost);
+      // chain level of every work item (fwd items then bwd items)
+      std::vector<int32_t> lev;
+      for (const ChainLayout* L : {&P->ch_f, &P->ch_b}) {
+        if (L->nbatch == 0)
+          continue;
+        std::vector<int32_t> bp((size_t)L->nbatch + 1), co((size_t)L->nchain),
+            cl((size_t)L->nchain);
+        cudaMemcpy(bp.data(), L->batch_ptr.p, sizeof(int32_t) * bp.size(), cudaMemcpyDeviceToHost);
+        cudaMemcpy(co.data(), L->corder.p, sizeof(int32_t) * co.size(), cudaMemcpyDeviceToHost);
+        cudaMemcpy(cl.data(), L->clevel.p, sizeof(int32_t) * cl.size(), cudaMemcpyDeviceToHost);
+        for (int32_t b = 0; b < L->nbatch; ++b)
+          lev.push_back(cl[(size_t)co[(size_t)bp[(size_t)b]]]);
+      }
       if (FILE* f = fopen(getenv("SFG_TRACE"), "wb")) {
         const int64_t hdr[3] = {items, P->trace_tiles, P->ch_f.nbatch};
         fwrite(hdr, sizeof(hdr), 1, f);
         fwrite(h.data(), sizeof(unsigned long long), h.size(), f);
+        fwrite(lev.data(), sizeof(int32_t), lev.size(), f);
         fclose(f);
       }
     }
