@@ -91,6 +91,12 @@ sfg_status sfg_plan_info(const sfg_plan* plan, int32_t* combo, int32_t* n,
 /* Replace the input vectors (st.vin = ...): nsys*n doubles, system-major,
  * host memory (pinned or pageable).  Asynchronous on the plan stream. */
 sfg_status sfg_set_vin(sfg_plan* plan, const double* vin_host);
+/* Replace the matrix values, same sparsity (make_state on a matrix with the
+ * pattern of the plan's, matrix.hpp:98-128): nsys*nnz(M) doubles in the
+ * plan_create layout.  Re-derives every numeric operand on the device; the
+ * inspection is kept.  Returns SFG_ERR_INVALID_MATRIX (zero diagonal) like
+ * plan creation for the combos that take lower(M).  Waits for the check. */
+sfg_status sfg_set_values(sfg_plan* plan, const double* values_host);
 
 /* Inspector (replaces build_g1/build_g2/inter_dag/joint_dag/level_info/
  * compute_reuse, dag.hpp:150-431, and msp + compile_schedule,

@@ -26,7 +26,7 @@ SFG_ERR_NO_DEVICE = 6
 EXPORTS = (
     "sfg_device_check", "sfg_version", "sfg_set_device", "sfg_host_alloc",
     "sfg_host_free", "sfg_bench_executions", "sfg_selftest_division", "sfg_plan_create", "sfg_plan_destroy",
-    "sfg_plan_set_stream", "sfg_plan_info", "sfg_set_vin", "sfg_inspect",
+    "sfg_plan_set_stream", "sfg_plan_info", "sfg_set_vin", "sfg_set_values", "sfg_inspect",
     "sfg_get_dag", "sfg_get_interdep", "sfg_get_levels", "sfg_compute_reuse",
     "sfg_get_schedule", "sfg_execute_fused", "sfg_execute_unfused",
     "sfg_synchronize", "sfg_collect_outputs", "sfg_device_output",
@@ -84,6 +84,8 @@ def load(path: str | None = None):
     L.sfg_plan_info.restype = st
     L.sfg_set_vin.argtypes = [vp, f64p]
     L.sfg_set_vin.restype = st
+    L.sfg_set_values.argtypes = [vp, f64p]
+    L.sfg_set_values.restype = st
     L.sfg_inspect.argtypes = [vp]
     L.sfg_inspect.restype = st
     L.sfg_get_dag.argtypes = [vp, C.c_int32, i32p, i64p, i32p, i32p, i64p]

@@ -145,6 +145,7 @@ class KernelState:
         self.combo = combo
         self.n = M.n
         self.nsys = nsys
+        self.nnz_m = int(M.nnz)
         cp = np.ascontiguousarray(M.colptr, np.int32)
         ri = np.ascontiguousarray(M.rowidx, np.int32)
         va = np.ascontiguousarray(M.values if values is None else values, np.float64)
@@ -186,6 +187,13 @@ class KernelState:
         if v.size != self.n * self.nsys:
             raise ValueError("vin must hold nsys * n doubles")
         self._chk(self.L.sfg_set_vin(self.h, ptr(v, f64p)), "set_vin")
+
+    def set_values(self, values: np.ndarray):
+        """New matrix values, same pattern (nsys * nnz(M), plan_create layout)."""
+        v = np.ascontiguousarray(values, np.float64)
+        if v.size != self.nnz_m * self.nsys:
+            raise ValueError("values must hold nsys * nnz(M) doubles")
+        self._chk(self.L.sfg_set_values(self.h, ptr(v, f64p)), "set_values")
 
     def set_stream(self, stream_handle: int | None):
         self._chk(self.L.sfg_plan_set_stream(self.h, stream_handle or None), "set_stream")

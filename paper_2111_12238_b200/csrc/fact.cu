@@ -1,0 +1,441 @@
+// fact.cu -- update-list inspector and warp-per-task executors for the
+// factorization pairs (combos 5, 6, 7).  See fact.cuh for the design.
+//
+// Arithmetic is the reference's bit for bit: every factor entry receives its
+// updates in the reference's order (predecessor column j ascending for IC0,
+// kernels.hpp:224-236; pivot k ascending for ILU0, kernels.hpp:253-268) with
+// separately rounded multiply and subtract, IEEE square root, and divisions
+// that are IEEE-exact (div_with_rcp falls back to the IEEE division outside
+// its proven range).
+#include <cub/cub.cuh>
+
+#include "common.cuh"
+#include "fact.cuh"
+
+namespace sfg {
+
+namespace {
+
+constexpr int kFBlock = 256;
+constexpr int CHU = 8;        // IC0: updates staged per lane per batch
+constexpr int kMaxIluUpd = 8;  // ILU0: updates a lane holds in registers
+constexpr unsigned FULL = 0xffffffffu;
+
+__device__ __forceinline__ double fsub_mul(double acc, double a, double b) {
+  return __dsub_rn(acc, __dmul_rn(a, b));
+}
+
+__device__ __forceinline__ double resolve(unsigned long long w, const double* p, unsigned cap) {
+  return is_sent_hi(w) ? poll_f64(p, cap) : __longlong_as_double((long long)w);
+}
+
+int grid_n(int64_t n) {
+  int64_t b = (n + kFBlock - 1) / kFBlock;
+  const int64_t cap = (int64_t)sm_count() * 16;
+  return (int)std::max<int64_t>(1, std::min(b, cap));
+}
+
+// ---------------------------------------------------------------------------
+// Inspector.  MODE 0 counts the updates of every factor position into cur[];
+// MODE 1 appends them at cur[target]++ (cur = exclusive scan of the counts).
+// One thread owns one task, i.e. every target position it writes, so the
+// lists come out in the task's loop order without atomics.
+// ---------------------------------------------------------------------------
+
+// IC0 column k: for each L(k,j) (row view q ascending = j ascending), the
+// rows of column j from k on that also occur in column k.
+template <int MODE>
+__global__ void k_ic0_updates(const int32_t* __restrict__ lc_ptr, const int32_t* __restrict__ lc_idx,
+                              const int32_t* __restrict__ rv_ptr, const int32_t* __restrict__ rv_col,
+                              const int32_t* __restrict__ rv_pos, int32_t n, int32_t* cur,
+                              int32_t* __restrict__ oa, int32_t* __restrict__ ob) {
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const int c0 = lc_ptr[k], c1 = lc_ptr[k + 1];
+    for (int q = rv_ptr[k]; q < rv_ptr[k + 1]; ++q) {
+      const int j = rv_col[q], pj = rv_pos[q], pe = lc_ptr[j + 1];
+      int a = c0;
+      for (int p = pj; p < pe && a < c1; ++p) {
+        const int i = lc_idx[p];
+        while (a < c1 && lc_idx[a] < i)
+          ++a;
+        if (a < c1 && lc_idx[a] == i) {
+          if (MODE == 0) {
+            ++cur[a];
+          } else {
+            const int e = cur[a]++;
+            oa[e] = p;  // fac[p] = L(i,j)
+            ob[e] = pj; // fac[pj] = L(k,j)
+          }
+        }
+      }
+    }
+  }
+}
+
+// ILU0 row i: for each lower entry k (pivot step t, ascending), the upper
+// entries U(k,j) of row k whose column j also occurs in row i after k.
+template <int MODE>
+__global__ void k_ilu0_updates(const int32_t* __restrict__ ar_ptr, const int32_t* __restrict__ ar_idx,
+                               const int32_t* __restrict__ diag, int32_t n, int32_t* cur,
+                               int32_t* __restrict__ oa, int32_t* __restrict__ ob) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int r0 = ar_ptr[i], r1 = ar_ptr[i + 1];
+    for (int pa = r0; pa < r1; ++pa) {
+      const int k = ar_idx[pa];
+      if (k >= i)
+        break;
+      const int dk = diag[k];
+      if (dk < 0) // missing pivot: reported by the executor
+        continue;
+      const int qe = ar_ptr[k + 1];
+      int b = pa + 1;
+      for (int q = dk + 1; q < qe && b < r1; ++q) {
+        const int j = ar_idx[q];
+        while (b < r1 && ar_idx[b] < j)
+          ++b;
+        if (b < r1 && ar_idx[b] == j) {
+          if (MODE == 0) {
+            ++cur[b];
+          } else {
+            const int e = cur[b]++;
+            oa[e] = pa - r0; // pivot step
+            ob[e] = q;       // fac[q] = U(k,j)
+          }
+        }
+      }
+    }
+  }
+}
+
+__global__ void k_list_stats(const int32_t* __restrict__ tptr, int32_t n,
+                             const int32_t* __restrict__ uptr, int64_t nnz, int32_t* out) {
+  int mt = 0, mu = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    mt = max(mt, tptr[i + 1] - tptr[i]);
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < nnz;
+       p += (int64_t)gridDim.x * blockDim.x)
+    mu = max(mu, uptr[p + 1] - uptr[p]);
+  atomicMax(out, mt);
+  atomicMax(out + 1, mu);
+}
+
+template <typename CountK, typename FillK>
+void build_lists(int32_t n, int64_t nnz, const int32_t* tptr, UpdateLists& out, cudaStream_t s,
+                 CountK count, FillK fill) {
+  DBuf<int32_t> cnt(nnz + 1);
+  SFG_CUDA(cudaMemsetAsync(cnt.p, 0, sizeof(int32_t) * (size_t)(nnz + 1), s));
+  count(cnt.p);
+  out.ptr.alloc(nnz + 1);
+  size_t bytes = 0;
+  SFG_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, bytes, cnt.p, out.ptr.p, nnz + 1, s));
+  {
+    DBuf<unsigned char> tmp((int64_t)bytes);
+    SFG_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, bytes, cnt.p, out.ptr.p, nnz + 1, s));
+  }
+  int32_t total = 0;
+  SFG_CUDA(cudaMemcpyAsync(&total, out.ptr.p + nnz, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+  SFG_CUDA(cudaStreamSynchronize(s));
+  out.count = total;
+  out.a.alloc(total > 0 ? total : 1);
+  out.b.alloc(total > 0 ? total : 1);
+  SFG_CUDA(cudaMemcpyAsync(cnt.p, out.ptr.p, sizeof(int32_t) * (size_t)(nnz + 1),
+                           cudaMemcpyDeviceToDevice, s));
+  fill(cnt.p, out.a.p, out.b.p);
+  DBuf<int32_t> st(2);
+  SFG_CUDA(cudaMemsetAsync(st.p, 0, sizeof(int32_t) * 2, s));
+  k_list_stats<<<grid_n(std::max<int64_t>(n, nnz)), kFBlock, 0, s>>>(tptr, n, out.ptr.p, nnz, st.p);
+  count_launch();
+  SFG_CUDA(cudaGetLastError());
+  int32_t h[2];
+  SFG_CUDA(cudaMemcpyAsync(h, st.p, sizeof(h), cudaMemcpyDeviceToHost, s));
+  SFG_CUDA(cudaStreamSynchronize(s));
+  out.max_task = h[0];
+  out.max_updates = h[1];
+}
+
+// ---------------------------------------------------------------------------
+// Executors.  One ticket = one task = one warp; lane a owns entry a of the
+// column (IC0) or row (ILU0).  Tasks are claimed in the inspector's level
+// order, so every producer a warp polls is already claimed (deadlock-free).
+// ---------------------------------------------------------------------------
+
+// IC0 column k (ic0_column, kernels.hpp:214-242), fused with the CSC-row
+// solve x_k (trsv_csc_row, kernels.hpp:200-210) for combo 5 or with DSCAL
+// applied on load (dscal_csc_col, kernels.hpp:281-286) for combo 7.
+//   src 0: column k from lc_val; 1: scaled on load; 2: pre-scaled in work.
+template <int COMBO>
+__global__ void __launch_bounds__(kFBlock) k_ic0_warp(const ExecArgs A,
+                                                      const int32_t* __restrict__ uptr,
+                                                      const int32_t* __restrict__ usrc,
+                                                      const int32_t* __restrict__ ulkj) {
+  const int lane = threadIdx.x & 31;
+  const int64_t total = A.t_end - A.t_begin;
+  const bool do_fac = COMBO == 5 ? (A.phase & 1) : (A.phase & 2);
+  const bool do_solve = COMBO == 5 && (A.phase & 2);
+  const int src = COMBO == 5 ? 0 : ((A.phase & 1) ? 1 : 2);
+  const int fac_kernel = COMBO == 5 ? 1 : 2;
+  const unsigned cap = A.sleep_cap;
+  for (;;) {
+    const long long c = claim_tickets(A.counter, 1);
+    if (c >= total)
+      break;
+    const int k = __ldg(A.order + A.t_begin + c);
+    const int c0 = __ldg(A.lc_ptr + k);
+    const int m = __ldg(A.lc_ptr + k + 1) - c0;
+    const int q0 = __ldg(A.rv_ptr + k);
+    const int q1 = __ldg(A.rv_ptr + k + 1);
+    // the solve's first 32 operands L(k,j), x_j: loads in flight during the
+    // factorization of column k
+    unsigned long long wl = 0, wx = 0;
+    int ql = -1, qx = -1;
+    if (do_solve && q0 + lane < q1) {
+      ql = __ldg(A.rv_pos + q0 + lane);
+      qx = __ldg(A.rv_col + q0 + lane);
+      wl = ld_relaxed_u64(A.fac + ql);
+      wx = ld_relaxed_u64(A.vout + qx);
+    }
+    double lkk;
+    if (do_fac) {
+      const int pa = c0 + lane;
+      double acc = 0.0;
+      int u0 = 0, u1 = 0;
+      if (lane < m) {
+        if (src == 0) {
+          acc = __ldg(A.lc_val + pa);
+        } else if (src == 1) {
+          const int row = __ldg(A.lc_idx + pa);
+          acc = __dmul_rn(__dmul_rn(__ldg(A.dvec + row), __ldg(A.lc_val + pa)), __ldg(A.dvec + k));
+        } else {
+          acc = __ldg(A.work + pa);
+        }
+        u0 = __ldg(uptr + pa);
+        u1 = __ldg(uptr + pa + 1);
+      }
+      for (int u = u0; u < u1; u += CHU) {
+        const int cnt = min(CHU, u1 - u);
+        int ps[CHU], pl[CHU];
+        unsigned long long ws[CHU], wk[CHU];
+#pragma unroll
+        for (int e = 0; e < CHU; ++e)
+          if (e < cnt) {
+            ps[e] = __ldg(usrc + u + e);
+            pl[e] = __ldg(ulkj + u + e);
+          }
+#pragma unroll
+        for (int e = 0; e < CHU; ++e)
+          if (e < cnt) {
+            ws[e] = ld_relaxed_u64(A.fac + ps[e]);
+            wk[e] = ld_relaxed_u64(A.fac + pl[e]);
+          }
+#pragma unroll
+        for (int e = 0; e < CHU; ++e)
+          if (e < cnt)
+            acc = fsub_mul(acc, resolve(wk[e], A.fac + pl[e], cap), resolve(ws[e], A.fac + ps[e], cap));
+      }
+      double l0 = 0.0;
+      if (lane == 0) {
+        if (acc <= 0.0)
+          report_error(A.err, fac_kernel, k, k);
+        l0 = __dsqrt_rn(acc);
+      }
+      lkk = __shfl_sync(FULL, l0, 0);
+      if (lane < m)
+        publish_f64(A.fac + pa, lane == 0 ? lkk : __ddiv_rn(acc, lkk));
+    } else {
+      lkk = do_solve ? poll_f64(A.fac + c0, cap) : 0.0;
+    }
+    if (do_solve) {
+      double acc2 = __ldg(A.vin + k);
+      for (int qb = q0; qb < q1; qb += 32) {
+        double lv = 0.0, xv = 0.0;
+        if (qb + lane < q1) {
+          if (qb != q0) {
+            ql = __ldg(A.rv_pos + qb + lane);
+            qx = __ldg(A.rv_col + qb + lane);
+            wl = ld_relaxed_u64(A.fac + ql);
+            wx = ld_relaxed_u64(A.vout + qx);
+          }
+          lv = resolve(wl, A.fac + ql, cap);
+          xv = resolve(wx, A.vout + qx, cap);
+        }
+        const int cnt = min(32, q1 - qb);
+        for (int t = 0; t < cnt; ++t)
+          acc2 = fsub_mul(acc2, __shfl_sync(FULL, lv, t), __shfl_sync(FULL, xv, t));
+      }
+      if (lane == 0) {
+        if (lkk == 0.0)
+          report_error(A.err, 2, k, k);
+        publish_f64(A.vout + k, __ddiv_rn(acc2, lkk));
+      }
+    }
+  }
+}
+
+// IKJ ILU0 row i (ilu0_row, kernels.hpp:246-272) fused with the unit-lower
+// solve y_i (trsv_csr_unit_row, kernels.hpp:184-196).  Pivot step t is the
+// t-th lower entry k_t of row i: lane t forms l_{i,k_t} = a_{i,k_t} / u_{k_t k_t}
+// once the updates of steps < t have reached it, the multiplier is broadcast,
+// and every lane holding a matching U(k_t, j) applies it.  The reciprocals of
+// all pivots are formed before the first step, off the serial chain.
+__global__ void __launch_bounds__(kFBlock) k_ilu0_warp(const ExecArgs A,
+                                                       const int32_t* __restrict__ uptr,
+                                                       const int32_t* __restrict__ ustep,
+                                                       const int32_t* __restrict__ usrc) {
+  const int lane = threadIdx.x & 31;
+  const int64_t total = A.t_end - A.t_begin;
+  const bool do_fac = A.phase & 1;
+  const bool do_solve = A.phase & 2;
+  const unsigned cap = A.sleep_cap;
+  for (;;) {
+    const long long c = claim_tickets(A.counter, 1);
+    if (c >= total)
+      break;
+    const int i = __ldg(A.order + A.t_begin + c);
+    const int r0 = __ldg(A.ar_ptr + i);
+    const int m = __ldg(A.ar_ptr + i + 1) - r0;
+    const int pb = r0 + lane;
+    const int col = lane < m ? __ldg(A.ar_idx + pb) : 0x7fffffff;
+    const bool lower = col < i;
+    const int nl = __popc(__ballot_sync(FULL, lower)); // lower lanes are 0 .. nl-1
+    unsigned long long wx = 0;
+    if (do_solve && lower)
+      wx = ld_relaxed_u64(A.vout + col);
+    double acc2 = do_solve ? __ldg(A.vin + i) : 0.0;
+    if (do_fac) {
+      double acc = lane < m ? __ldg(A.ar_val + pb) : 0.0;
+      const int dk = lower ? __ldg(A.diag + col) : -1;
+      unsigned long long wp = 0;
+      if (dk >= 0)
+        wp = ld_relaxed_u64(A.fac + dk);
+      int nu = 0, ub = 0;
+      if (lane < m) {
+        ub = __ldg(uptr + pb);
+        nu = __ldg(uptr + pb + 1) - ub;
+      }
+      int st[kMaxIluUpd];
+      int sq[kMaxIluUpd];
+      unsigned long long wu[kMaxIluUpd];
+#pragma unroll
+      for (int e = 0; e < kMaxIluUpd; ++e) {
+        st[e] = -1;
+        if (e < nu) {
+          st[e] = __ldg(ustep + ub + e);
+          sq[e] = __ldg(usrc + ub + e);
+        }
+      }
+#pragma unroll
+      for (int e = 0; e < kMaxIluUpd; ++e)
+        if (e < nu)
+          wu[e] = ld_relaxed_u64(A.fac + sq[e]);
+      double uv[kMaxIluUpd];
+#pragma unroll
+      for (int e = 0; e < kMaxIluUpd; ++e)
+        uv[e] = e < nu ? resolve(wu[e], A.fac + sq[e], cap) : 0.0;
+      const double piv = dk >= 0 ? resolve(wp, A.fac + dk, cap) : 0.0;
+      const double rcp = __drcp_rn(piv);
+      const double xk = do_solve && lower ? resolve(wx, A.vout + col, cap) : 0.0;
+      for (int t = 0; t < nl; ++t) {
+        if (lane == t) {
+          if (dk < 0 || piv == 0.0)
+            report_error(A.err, 1, i, col);
+          acc = div_with_rcp(acc, piv, rcp);
+        }
+        const double lik = __shfl_sync(FULL, acc, t);
+#pragma unroll
+        for (int e = 0; e < kMaxIluUpd; ++e)
+          if (st[e] == t)
+            acc = fsub_mul(acc, lik, uv[e]);
+        if (do_solve)
+          acc2 = fsub_mul(acc2, lik, __shfl_sync(FULL, xk, t));
+      }
+      if (lane < m)
+        publish_f64(A.fac + pb, acc);
+    } else if (do_solve) { // unit solve alone (unfused second launch)
+      double lv = 0.0, xk = 0.0;
+      if (lower) {
+        lv = poll_f64(A.fac + pb, cap);
+        xk = resolve(wx, A.vout + col, cap);
+      }
+      for (int t = 0; t < nl; ++t)
+        acc2 = fsub_mul(acc2, __shfl_sync(FULL, lv, t), __shfl_sync(FULL, xk, t));
+    }
+    if (do_solve && lane == 0)
+      publish_f64(A.vout + i, acc2);
+  }
+}
+
+template <typename K> void launch_warp_tasks(K kernel, const ExecArgs& a, const UpdateLists& up,
+                                             cudaStream_t s) {
+  const int64_t total = a.t_end - a.t_begin;
+  if (total <= 0)
+    return;
+  int per_sm = 0;
+  SFG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kFBlock, 0));
+  per_sm = std::max(per_sm, 1);
+  if (a.blocks_per_sm > 0 && a.blocks_per_sm < per_sm)
+    per_sm = a.blocks_per_sm;
+  int64_t blocks = (total + (kFBlock / 32) - 1) / (kFBlock / 32);
+  blocks = std::min<int64_t>(blocks, (int64_t)per_sm * sm_count());
+  kernel<<<(unsigned)blocks, kFBlock, 0, s>>>(a, up.ptr.p, up.a.p, up.b.p);
+  count_launch();
+  SFG_CUDA(cudaGetLastError());
+}
+
+} // namespace
+
+void build_ic0_updates(const int32_t* lc_ptr, const int32_t* lc_idx, const int32_t* rv_ptr,
+                       const int32_t* rv_col, const int32_t* rv_pos, int32_t n, int64_t nnz,
+                       UpdateLists& out, cudaStream_t s) {
+  const int g = grid_n(n);
+  build_lists(
+      n, nnz, lc_ptr, out, s,
+      [&](int32_t* cnt) {
+        k_ic0_updates<0><<<g, kFBlock, 0, s>>>(lc_ptr, lc_idx, rv_ptr, rv_col, rv_pos, n, cnt,
+                                               nullptr, nullptr);
+        count_launch();
+        SFG_CUDA(cudaGetLastError());
+      },
+      [&](int32_t* cur, int32_t* oa, int32_t* ob) {
+        k_ic0_updates<1><<<g, kFBlock, 0, s>>>(lc_ptr, lc_idx, rv_ptr, rv_col, rv_pos, n, cur, oa, ob);
+        count_launch();
+        SFG_CUDA(cudaGetLastError());
+      });
+}
+
+void build_ilu0_updates(const int32_t* ar_ptr, const int32_t* ar_idx, const int32_t* diag,
+                        int32_t n, int64_t nnz, UpdateLists& out, cudaStream_t s) {
+  const int g = grid_n(n);
+  build_lists(
+      n, nnz, ar_ptr, out, s,
+      [&](int32_t* cnt) {
+        k_ilu0_updates<0><<<g, kFBlock, 0, s>>>(ar_ptr, ar_idx, diag, n, cnt, nullptr, nullptr);
+        count_launch();
+        SFG_CUDA(cudaGetLastError());
+      },
+      [&](int32_t* cur, int32_t* oa, int32_t* ob) {
+        k_ilu0_updates<1><<<g, kFBlock, 0, s>>>(ar_ptr, ar_idx, diag, n, cur, oa, ob);
+        count_launch();
+        SFG_CUDA(cudaGetLastError());
+      });
+}
+
+bool ic0_warp_fits(const UpdateLists& up) { return up.max_task <= 32; }
+bool ilu0_warp_fits(const UpdateLists& up) {
+  return up.max_task <= 32 && up.max_updates <= kMaxIluUpd;
+}
+
+void launch_ic0_warp(int combo, const ExecArgs& a, const UpdateLists& up, cudaStream_t s) {
+  if (combo == 5)
+    launch_warp_tasks(k_ic0_warp<5>, a, up, s);
+  else
+    launch_warp_tasks(k_ic0_warp<7>, a, up, s);
+}
+
+void launch_ilu0_warp(const ExecArgs& a, const UpdateLists& up, cudaStream_t s) {
+  launch_warp_tasks(k_ilu0_warp, a, up, s);
+}
+
+} // namespace sfg

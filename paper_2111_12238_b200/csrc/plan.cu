@@ -5,6 +5,7 @@
 #include "../../include/sfgpu.h"
 #include "chain.cuh"
 #include "ell.cuh"
+#include "fact.cuh"
 #include "common.cuh"
 #include "executor.cuh"
 #include "internal.hpp"
@@ -43,6 +44,9 @@ struct sfg_plan {
   DBuf<int32_t> lc_ptr, lc_idx, rv_ptr, rv_col, rv_pos;
   DBuf<double> lc_val, dvec;
   DBuf<double> vin, vmid, vout, fac, work, staging;
+  // value maps (positions in M) kept for sfg_set_values
+  DBuf<int32_t> map_lc, map_lr, map_lt, map_ar;
+  DBuf<double> mstage;
 
   // schedule
   bool inspected = false;
@@ -70,6 +74,9 @@ struct sfg_plan {
   std::vector<int32_t> row_maxcol; // (unused by the chain path; kept for stats)
   int32_t tile_rows = 0;           // chain tile height override (S == 1)
   DBuf<unsigned long long> trace;  // SFG_TRACE diagnostics
+  // warp-per-task factorization executors (combos 5, 6, 7)
+  bool use_warpfac = false;
+  UpdateLists upd;
   int32_t trace_tiles = 0;
 
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
@@ -411,6 +418,9 @@ void build_plan(sfg_plan* P, const int32_t* colptr, const int32_t* rowidx,
     const int64_t nnzL = P->nnzL;
     if (combo == 5 || combo == 7)
       values_from(mval, nnzM, S, src.p, nnzL, P->lc_val, s);
+    P->map_lc.alloc(nnzL > 0 ? nnzL : 1);
+    SFG_CUDA(cudaMemcpyAsync(P->map_lc.p, src.p, sizeof(int32_t) * (size_t)nnzL,
+                             cudaMemcpyDeviceToDevice, s));
     // CSR of L: to_csr (matrix.hpp:66-86), rows ascending columns, diag last
     DBuf<int32_t> csr_ptr((int64_t)n + 1), csr_idx(nnzL > 0 ? nnzL : 1),
         perm(nnzL > 0 ? nnzL : 1), srcc(nnzL > 0 ? nnzL : 1);
@@ -419,6 +429,8 @@ void build_plan(sfg_plan* P, const int32_t* colptr, const int32_t* rowidx,
       compose_kernel<<<grid_for(nnzL), 256, 0, s>>>(src.p, perm.p, nnzL, srcc.p);
       count_launch();
       values_from(mval, nnzM, S, srcc.p, nnzL, P->lr_val, s);
+      P->map_lr = std::move(srcc);
+      srcc.alloc(nnzL > 0 ? nnzL : 1);
       P->lr_ptr = std::move(csr_ptr);
       P->lr_idx = std::move(csr_idx);
     } else {
@@ -444,6 +456,7 @@ void build_plan(sfg_plan* P, const int32_t* colptr, const int32_t* rowidx,
       compose_kernel<<<grid_for(nnzL), 256, 0, s>>>(src.p, rperm.p, nnzL, srcc.p);
       count_launch();
       values_from(mval, nnzM, S, srcc.p, nnzL, P->lt_val, s);
+      P->map_lt = std::move(srcc);
     }
     if (combo == 4) {
       // CSR view of the CSC SpMV operand A = M (row gather, see executor.cu)
@@ -452,6 +465,7 @@ void build_plan(sfg_plan* P, const int32_t* colptr, const int32_t* rowidx,
       DBuf<int32_t> aperm(nnzM > 0 ? nnzM : 1);
       transpose(P->m_ptr.p, P->m_idx.p, n, n, nnzM, P->ar_ptr.p, P->ar_idx.p, aperm.p, s);
       values_from(mval, nnzM, 1, aperm.p, nnzM, P->ar_val, s);
+      P->map_ar = std::move(aperm);
     }
     if (combo == 7) {
       P->dvec.alloc(n > 0 ? n : 1);
@@ -469,6 +483,7 @@ void build_plan(sfg_plan* P, const int32_t* colptr, const int32_t* rowidx,
     DBuf<int32_t> aperm(nnzM > 0 ? nnzM : 1);
     transpose(P->m_ptr.p, P->m_idx.p, n, n, nnzM, P->ar_ptr.p, P->ar_idx.p, aperm.p, s);
     values_from(mval, nnzM, 1, aperm.p, nnzM, P->ar_val, s);
+    P->map_ar = std::move(aperm);
     P->diag.alloc(n > 0 ? n : 1);
     find_diag_positions(P->ar_ptr.p, P->ar_idx.p, n, P->diag.p, s);
     P->nnzF = nnzM;
@@ -559,10 +574,16 @@ void launch_main(sfg_plan* P, const ExecArgs& a) {
     break;
   case 5:
   case 7:
-    launch_ic0(P->combo, a, P->stream);
+    if (P->use_warpfac)
+      launch_ic0_warp(P->combo, a, P->upd, P->stream);
+    else
+      launch_ic0(P->combo, a, P->stream);
     break;
   case 6:
-    launch_ilu0(a, P->stream);
+    if (P->use_warpfac)
+      launch_ilu0_warp(a, P->upd, P->stream);
+    else
+      launch_ilu0(a, P->stream);
     break;
   }
 }
@@ -613,10 +634,20 @@ void do_inspect(sfg_plan* P) {
     for (size_t k = 1; k < w2.size(); ++k)
       P->wave_ptr.push_back(w2[k] + n);
   }
-  if (combo == 1 || combo == 4 || combo == 8) {
-    const char* ex = getenv("SFG_EXECUTOR");
-    P->use_chain = !(ex && std::string(ex) == "levels");
+  const char* ex = getenv("SFG_EXECUTOR");
+  const bool legacy = ex && std::string(ex) == "levels";
+  if (combo == 1 || combo == 4 || combo == 8)
+    P->use_chain = !legacy;
+  if (!legacy && (combo == 5 || combo == 7)) {
+    build_ic0_updates(P->lc_ptr.p, P->lc_idx.p, P->rv_ptr.p, P->rv_col.p, P->rv_pos.p, n,
+                      P->nnzF, P->upd, s);
+    P->use_warpfac = ic0_warp_fits(P->upd);
+  } else if (!legacy && combo == 6) {
+    build_ilu0_updates(P->ar_ptr.p, P->ar_idx.p, P->diag.p, n, P->nnzF, P->upd, s);
+    P->use_warpfac = ilu0_warp_fits(P->upd);
   }
+  if (!P->use_warpfac)
+    P->upd = UpdateLists{};
   if (P->use_chain) {
     if (const char* e = getenv("SFG_CHAIN_G"))
       P->tile_rows = atoi(e);
@@ -1241,6 +1272,75 @@ sfg_status sfg_set_vin(sfg_plan* P, const double* vin_host) {
                                cudaMemcpyHostToDevice, P->stream));
       interleave(P->staging.p, P->n, P->nsys, P->vin.p, P->stream);
     }
+    return SFG_OK;
+  });
+}
+
+namespace {
+
+// Zero diagonal of any system (lower_triangle's check, matrix.hpp:106-112):
+// L_csc keeps the diagonal first in every column.
+__global__ void diag_check_kernel(const double* __restrict__ mval, int64_t nnzM, int32_t S,
+                                  const int32_t* __restrict__ lptr, const int32_t* __restrict__ map,
+                                  int32_t n, unsigned long long* bad) {
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < (int64_t)n * S;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t j = (int32_t)(t / S), sys = (int32_t)(t % S);
+    if (mval[(int64_t)sys * nnzM + map[lptr[j]]] == 0.0)
+      atomicMin(bad, (unsigned long long)j << 1);
+  }
+}
+
+} // namespace
+
+sfg_status sfg_set_values(sfg_plan* P, const double* values_host) {
+  if (!P || !values_host)
+    return SFG_ERR_INVALID_ARGUMENT;
+  return guarded(P, [&] {
+    DeviceScope ds(P->device);
+    LaunchScope ls(P);
+    cudaStream_t s = P->stream;
+    const int32_t n = P->n, S = P->nsys;
+    const int64_t nnzM = P->nnzM, tot = nnzM * S;
+    if (tot == 0)
+      return SFG_OK;
+    if (P->mstage.n < tot)
+      P->mstage.alloc(tot);
+    SFG_CUDA(cudaMemcpyAsync(P->mstage.p, values_host, sizeof(double) * (size_t)tot,
+                             cudaMemcpyHostToDevice, s));
+    const int c = P->combo;
+    if (c != 6) {
+      DBuf<unsigned long long> bad(1);
+      SFG_CUDA(cudaMemsetAsync(bad.p, 0xFF, sizeof(unsigned long long), s));
+      diag_check_kernel<<<grid_for((int64_t)n * S), 256, 0, s>>>(P->mstage.p, nnzM, S,
+                                                                  P->lc_ptr.p, P->map_lc.p, n,
+                                                                  bad.p);
+      count_launch();
+      SFG_CUDA(cudaGetLastError());
+      unsigned long long hbad = 0;
+      SFG_CUDA(cudaMemcpyAsync(&hbad, bad.p, sizeof(hbad), cudaMemcpyDeviceToHost, s));
+      SFG_CUDA(cudaStreamSynchronize(s));
+      if (hbad != ~0ull) {
+        const int32_t j = (int32_t)(hbad >> 1);
+        throw InvalidMatrix("zero diagonal entry at column " + std::to_string(j), j);
+      }
+    }
+    const int64_t nnzL = P->nnzL;
+    if (c == 1 || c == 4 || c == 8)
+      gather_values(P->mstage.p, nnzM, P->map_lr.p, nnzL, S, P->lr_val.p, s);
+    if (c == 8)
+      gather_values(P->mstage.p, nnzM, P->map_lt.p, nnzL, S, P->lt_val.p, s);
+    if (c == 5 || c == 7)
+      gather_values(P->mstage.p, nnzM, P->map_lc.p, nnzL, S, P->lc_val.p, s);
+    if (c == 4 || c == 6)
+      gather_values(P->mstage.p, nnzM, P->map_ar.p, nnzM, 1, P->ar_val.p, s);
+    if (c == 7)
+      dscal_vector(P->lc_ptr.p, P->lc_val.p, n, P->dvec.p, s);
+    if (P->use_ell) { // the chain-ELL records hold copies of the values
+      build_ell(P->lr_ptr.p, P->lr_idx.p, P->lr_val.p, n, S, +1, P->ell_chn, P->ch_f, P->ell_f, s);
+      build_ell(P->lt_ptr.p, P->lt_idx.p, P->lt_val.p, n, S, -1, P->ell_chn, P->ch_b, P->ell_b, s);
+    }
+    SFG_CUDA(cudaGetLastError());
     return SFG_OK;
   });
 }

@@ -248,3 +248,41 @@ def test_division_from_reciprocal_is_ieee():
     assert abi.load().sfg_selftest_division(n, 12345, C.byref(bad), C.byref(fast)) == 0
     assert bad.value == 0
     assert fast.value > n // 10
+
+
+@pytest.mark.parametrize("combo", GPU_COMBOS)
+def test_set_values_refactorizes(orc, golden, combo):
+    # new values, same pattern: equals a fresh state built on those values
+    Mo = golden_matrix(golden, "grid10")
+    st = sf.make_state(combo, as_sf(Mo), seed=7).inspect()
+    st.execute_fused()
+    v2 = Mo.values * 1.25
+    st.set_values(v2)
+    st.execute_fused()
+    want = orc.run_sequential(combo, Csc(Mo.n, Mo.colptr, Mo.rowidx, v2), 7)
+    assert np.array_equal(st.collect_outputs(), want)
+    st.execute_unfused()
+    assert np.array_equal(st.collect_outputs(), want)
+
+
+def test_set_values_full_size_config4(orc):
+    M = sf.config_matrix(4)
+    st = sf.make_state(7, M, seed=7).inspect()
+    v2 = M.values.copy()
+    v2[M.rowidx == np.repeat(np.arange(M.n), np.diff(M.colptr))] *= 2.0  # heavier diagonal
+    st.set_values(v2)
+    st.execute_fused()
+    want = orc.run_sequential(7, Csc(M.n, M.colptr, M.rowidx, v2), 7)
+    assert np.array_equal(st.collect_outputs(), want)
+
+
+@pytest.mark.parametrize("combo", (1, 5, 7, 8))
+def test_set_values_zero_diagonal(golden, combo):
+    Mo = golden_matrix(golden, "grid6")
+    st = sf.make_state(combo, as_sf(Mo))
+    v2 = Mo.values.copy()
+    j = 4
+    p = Mo.colptr[j] + list(Mo.rowidx[Mo.colptr[j]:Mo.colptr[j + 1]]).index(j)
+    v2[p] = 0.0
+    with pytest.raises(sf.InvalidMatrixError, match="zero diagonal entry at column 4"):
+        st.set_values(v2)
