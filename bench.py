@@ -171,6 +171,22 @@ def algorithmic_bytes(cfg: int, n: int, nnzL: int, nnzA: int) -> int:
     raise ValueError(cfg)
 
 
+def physical_bytes(cfg: int, n: int, nnzL: int, nnzA: int, S: int) -> int:
+    """Bytes the executor must move at least (config 5: each system's L values
+    streamed by both solves, the shared pattern twice, b read, z written and
+    re-read, x written); the other configs equal the algorithmic bytes."""
+    if cfg != 5:
+        return algorithmic_bytes(cfg, n, nnzL, nnzA)
+    ptr = 4 * (n + 1)
+    return S * (2 * 8 * nnzL + 4 * 8 * n) + 2 * (4 * nnzL + ptr)
+
+
+def kernel_name(cfg: int, combo: int, S: int) -> str:
+    return {8: f"k_chain_sm<{S},4,12,8> (fwd L + bwd L^T)", 1: f"k_chain_sm<{S},4,12,1>",
+            4: "k_chain<1,...,4> (fwd L + SpMV tails)", 5: "k_ic0_warp<5>",
+            6: "k_ilu0_warp", 7: "k_ic0_warp<7>"}.get(combo, f"combo {combo} executor")
+
+
 def lower_nnz(M) -> int:
     cols = np.repeat(np.arange(M.n, dtype=np.int64), np.diff(M.colptr))
     return int(np.count_nonzero(M.rowidx >= cols))
@@ -317,7 +333,10 @@ def run_ours(args, D: Dist):
                      "frac": achieved / peak, "traffic": ncu_traffic(workload),
                      "peak_source": peak_src, "kernel_ms": kernel_ms,
                      "algorithmic_bytes_per_launch": bytes_per_launch,
-                     "kernel": "k_trsv_pair<8,8>" if combo == 8 else f"combo {combo} executor"},
+                     "kernel": kernel_name(cfg, combo, S),
+                     "physical_bytes_per_launch": physical_bytes(cfg, M.n, nnzL, M.nnz, S),
+                     "physical_frac": physical_bytes(cfg, M.n, nnzL, M.nnz, S)
+                     / (kernel_ms / 1e3) / 1e9 / peak},
         "unfused": {"ms_per_step": u_ms, "value": S * D.world / (u_ms / 1e3),
                     "fused_speedup": u_ms / ms_step},
         "e2e": e2e,
