@@ -1,0 +1,484 @@
+// mline.cu -- inspector and executor of the multi-chain warp scheme (see
+// mline.cuh).
+#include "common.cuh"
+#include "mline.cuh"
+
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
+
+namespace sfg {
+
+namespace {
+
+constexpr unsigned FULL = 0xffffffffu;
+constexpr int kMThreads = 128; // 4 warps per CTA
+constexpr int QC = 5;          // meta / code slots: steps i .. i+4
+constexpr int QV = 4;          // value / rhs slots: steps i .. i+3
+constexpr int QX = 3;          // gathered x slots: steps i .. i+2
+
+inline unsigned mgrid(int64_t work, int block = 256) {
+  int64_t g = (work + block - 1) / block;
+  const int64_t cap = (int64_t)sm_count() * 32;
+  if (g > cap)
+    g = cap;
+  return (unsigned)(g < 1 ? 1 : g);
+}
+
+__device__ __forceinline__ int pos_of(int j, int n, int dir) { return dir > 0 ? j : n - 1 - j; }
+
+// ---------------------------------------------------------------------------
+// inspector
+// ---------------------------------------------------------------------------
+
+// One thread per group: skews of its chains in order (an earlier chain's
+// skew is final before a later chain reads it) and the group's step count.
+__global__ void group_skew_kernel(const int32_t* __restrict__ ptr, const int32_t* __restrict__ idx,
+                                  int32_t n, int dir, const int32_t* __restrict__ cstart,
+                                  const int32_t* __restrict__ chain_of, int32_t nchain, int32_t B,
+                                  int32_t ngroup, int32_t* cskew, int32_t* __restrict__ gsteps) {
+  for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < ngroup;
+       g += (int64_t)gridDim.x * blockDim.x) {
+    const int c0 = (int)g * B;
+    const int nb = min(B, nchain - c0);
+    const int gp0 = cstart[c0];
+    int T = 0;
+    for (int b = 0; b < nb; ++b) {
+      const int c = c0 + b;
+      const int p0 = cstart[c];
+      const int len = cstart[c + 1] - p0;
+      int sk = 0;
+      for (int o = 0; o < len; ++o) {
+        const int p = p0 + o;
+        const int r = dir > 0 ? p : n - 1 - p;
+        const int e1 = ptr[r + 1] - 1;
+        for (int e = ptr[r]; e < e1; ++e) {
+          const int pj = pos_of(idx[e], n, dir);
+          if (pj >= gp0 && pj < p0) {
+            const int cj = chain_of[pj];
+            const int need = cskew[cj] + (pj - cstart[cj]) - o + 1;
+            sk = need > sk ? need : sk;
+          }
+        }
+      }
+      cskew[c] = sk;
+      T = sk + len > T ? sk + len : T;
+    }
+    gsteps[g] = T;
+  }
+}
+
+// One thread per position: dependency codes (ring or external) and the
+// group-DAG edge keys (group << 32 | dependency group; all-ones if internal).
+__global__ void codes_kernel(const int32_t* __restrict__ ptr, const int32_t* __restrict__ idx,
+                             int32_t n, int dir, const int32_t* __restrict__ cstart,
+                             const int32_t* __restrict__ chain_of, const int32_t* __restrict__ cskew,
+                             int32_t B, int32_t* __restrict__ code, uint64_t* __restrict__ keys,
+                             int* width) {
+  int wmax = 0;
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n;
+       p += (int64_t)gridDim.x * blockDim.x) {
+    const int c = chain_of[p];
+    const int g = c / B;
+    const int c0 = g * B;
+    const int gp0 = cstart[c0];
+    const int o = (int)p - cstart[c];
+    const int step = cskew[c] + o;
+    const int r = dir > 0 ? (int)p : n - 1 - (int)p;
+    const int e0 = ptr[r], e1 = ptr[r + 1] - 1;
+    const int nd = e1 - e0 - (o > 0 ? 1 : 0);
+    wmax = nd > wmax ? nd : wmax;
+    for (int e = e0; e < e1; ++e) {
+      const int j = idx[e];
+      const int pj = pos_of(j, n, dir);
+      int cd = j;
+      uint64_t key = ~0ull;
+      if (pj >= gp0) {
+        const int cj = chain_of[pj];
+        const int delta = step - (cskew[cj] + (pj - cstart[cj]));
+        if (delta >= 1 && delta < kRing)
+          cd = -1 - (delta * 32 + (cj - c0));
+      } else {
+        const int gj = chain_of[pj] / B;
+        key = ((uint64_t)(uint32_t)g << 32) | (uint32_t)gj;
+      }
+      code[e] = cd;
+      keys[e] = key;
+    }
+    code[e1] = r;
+    keys[e1] = ~0ull;
+  }
+  atomicMax(width, wmax);
+}
+
+// ---------------------------------------------------------------------------
+// executor
+// ---------------------------------------------------------------------------
+
+template <int S, int CHN> struct MlWarp {
+  static constexpr int B = 32 / S;
+  int32_t code[QC][B][CHN];
+  int32_t meta[QC][B][4]; // row (-1 = idle), first dependency entry, #deps, chained
+  int32_t rptr[3][B][2];  // row pointers of steps i+4 .. i+6
+  double v[QV][B][CHN + 2][S]; // deps, carry coefficient, diagonal
+  unsigned long long x[QX][B][CHN][S];
+  unsigned long long rhs[QV][B][S];
+  double ring[kRing][32];
+};
+
+__device__ __forceinline__ void cp8(void* dst, const void* src) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp4(void* dst, const void* src) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(d), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+__device__ __forceinline__ void cp_wait0() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
+template <int S, int CHN>
+__global__ void __launch_bounds__(kMThreads) k_mline(const MLineArgs A) {
+  constexpr int B = 32 / S;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  MlWarp<S, CHN>& W = reinterpret_cast<MlWarp<S, CHN>*>(smem_raw)[threadIdx.x >> 5];
+  const int lane = threadIdx.x & 31;
+  const int b = lane / S;
+  const int s = lane % S;
+  const int total = A.seg_end - A.seg_begin;
+  for (;;) {
+    unsigned long long w0 = 0;
+    if (lane == 0)
+      w0 = atomicAdd(A.counter, 1ull);
+    const long long wi = (long long)__shfl_sync(FULL, w0, 0);
+    if (wi >= total)
+      break;
+    const int item = A.seg_begin + (int)wi;
+    const bool second = item >= A.f_ngroup;
+    const bool bwd = second && A.combo == 8;
+    const int32_t* ptr = bwd ? A.lt_ptr : A.lr_ptr;
+    const double* val = bwd ? A.lt_val : A.lr_val;
+    const int32_t* code = bwd ? A.b_code : A.f_code;
+    const int32_t* cstart = bwd ? A.b_cstart : A.f_cstart;
+    const int32_t* cskew = bwd ? A.b_cskew : A.f_cskew;
+    const int nchain = bwd ? A.b_nchain : A.f_nchain;
+    const int g = second ? __ldg((bwd ? A.b_gorder : A.f_gorder) + (item - A.f_ngroup))
+                         : __ldg(A.f_gorder + item);
+    const int T = __ldg((bwd ? A.b_gsteps : A.f_gsteps) + g);
+    const int c = g * B + b;
+    const bool has_chain = c < nchain;
+    const int p0 = has_chain ? __ldg(cstart + c) : 0;
+    const int len = has_chain ? __ldg(cstart + c + 1) - p0 : 0;
+    const int skew = has_chain ? __ldg(cskew + c) : 0;
+    double* xo = second ? A.vout : A.vmid;
+    const double* rhs_vec = second ? A.vmid : A.vin;
+    const int kern = second ? 2 : 1;
+    auto row_of = [&](int o) {
+      const int p = p0 + o;
+      return bwd ? A.n - 1 - p : p;
+    };
+    double carry = 0.0;
+    unsigned long long tr_claim = 0, tr_first = 0, wait_cyc = 0, poll_cyc = 0;
+    if (A.trace)
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tr_claim));
+    __syncwarp();
+    // Every global operand reaches shared memory through cp.async, one
+    // commit group per iteration, so no load result is carried across
+    // iterations in a register (a register hand-off would stall the warp on
+    // the load at the end of every step).
+#pragma unroll 1
+    for (int i = -6; i < T; ++i) {
+      if (A.trace && i == 0)
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tr_first));
+      // groups <= i-2 complete: row pointers of step i+4, codes of step i+2,
+      // values of step i+1 and gathered x of step i
+      const long long wc0 = A.trace ? clock64() : 0;
+      cp_wait1();
+      __syncwarp();
+      if (A.trace)
+        wait_cyc += clock64() - wc0;
+      // ---- stage A: row pointers of step i+6
+      {
+        const int o = i + 6 - skew;
+        if (s == 0 && o >= 0 && o < len) {
+          const int r = row_of(o);
+          cp4(&W.rptr[(i + 6) % 3][b][0], ptr + r);
+          cp4(&W.rptr[(i + 6) % 3][b][1], ptr + r + 1);
+        }
+      }
+      // ---- stage B': meta + dependency codes of step i+4
+      if (i + 4 >= 0) {
+        const int q = (i + 4) % QC;
+        const int o = i + 4 - skew;
+        const bool act = o >= 0 && o < len;
+        const bool chained = o > 0;
+        const int r = act ? row_of(o) : -1;
+        const int e0 = act ? W.rptr[(i + 4) % 3][b][0] : 0;
+        const int e1 = act ? W.rptr[(i + 4) % 3][b][1] : 0;
+        const int nd = act ? e1 - e0 - 1 - (chained ? 1 : 0) : 0;
+        if (s == 0) {
+          W.meta[q][b][0] = r;
+          W.meta[q][b][1] = e0;
+          W.meta[q][b][2] = nd;
+          W.meta[q][b][3] = chained ? 1 : 0;
+        }
+        if (act) {
+          const int m = nd < CHN ? nd : CHN;
+          for (int a = s; a < m; a += S)
+            cp4(&W.code[q][b][a], code + e0 + a);
+        }
+      }
+      __syncwarp();
+      // ---- stage B: values and right-hand side of step i+3
+      if (i + 3 >= 0) {
+        const int q = (i + 3) % QC;
+        const int qv = (i + 3) % QV;
+        const int r = W.meta[q][b][0];
+        if (r >= 0) {
+          const int e0 = W.meta[q][b][1];
+          const int nd = W.meta[q][b][2];
+          const bool chained = W.meta[q][b][3] != 0;
+          const int m = nd < CHN ? nd : CHN;
+          const double* vb = val + (size_t)e0 * S + s;
+#pragma unroll
+          for (int a = 0; a < CHN; ++a)
+            if (a < m)
+              cp8(&W.v[qv][b][a][s], vb + (size_t)a * S);
+          const int ediag = e0 + nd + (chained ? 1 : 0);
+          if (chained)
+            cp8(&W.v[qv][b][CHN][s], val + (size_t)(ediag - 1) * S + s);
+          cp8(&W.v[qv][b][CHN + 1][s], val + (size_t)ediag * S + s);
+          cp8(&W.rhs[qv][b][s], rhs_vec + (size_t)r * S + s);
+        }
+      }
+      // ---- stage C: gather the external x words of step i+2
+      if (i + 2 >= 0) {
+        const int q = (i + 2) % QC;
+        const int qx = (i + 2) % QX;
+        if (W.meta[q][b][0] >= 0) {
+          const int nd = W.meta[q][b][2];
+          const int m = nd < CHN ? nd : CHN;
+#pragma unroll
+          for (int a = 0; a < CHN; ++a)
+            if (a < m) {
+              const int cd = W.code[q][b][a];
+              if (cd >= 0)
+                cp8(&W.x[qx][b][a][s], xo + (size_t)cd * S + s);
+            }
+        }
+      }
+      cp_commit();
+      // ---- stage D: row of step i
+      if (i >= 0) {
+        const int q = i % QC;
+        const int qv = i % QV;
+        const int qx = i % QX;
+        const int r = W.meta[q][b][0];
+        if (r >= 0) {
+          const int e0 = W.meta[q][b][1];
+          const int nd = W.meta[q][b][2];
+          const bool chained = W.meta[q][b][3] != 0;
+          const int m = nd < CHN ? nd : CHN;
+          const double d = W.v[qv][b][CHN + 1][s];
+          const double rd = __drcp_rn(d);
+          unsigned long long rw = W.rhs[qv][b][s];
+          int cds[CHN];
+          unsigned long long wd[CHN];
+#pragma unroll
+          for (int a = 0; a < CHN; ++a)
+            if (a < m) {
+              const int cd = W.code[q][b][a];
+              cds[a] = cd;
+              if (cd >= 0) {
+                wd[a] = W.x[qx][b][a][s];
+              } else {
+                const int t = -1 - cd;
+                wd[a] = (unsigned long long)__double_as_longlong(
+                    W.ring[(i - (t >> 5)) & (kRing - 1)][(t & 31) * S + s]);
+              }
+            }
+          // re-poll words that were still unpublished when gathered
+          const long long pc0 = A.trace ? clock64() : 0;
+          for (;;) {
+            bool pending = is_sent_hi(rw);
+#pragma unroll
+            for (int a = 0; a < CHN; ++a)
+              pending |= a < m && is_sent_hi(wd[a]);
+            if (!pending)
+              break;
+            if (A.sleep_ns)
+              __nanosleep(A.sleep_ns);
+            if (is_sent_hi(rw))
+              rw = ld_relaxed_u64(rhs_vec + (size_t)r * S + s);
+#pragma unroll
+            for (int a = 0; a < CHN; ++a)
+              if (a < m && is_sent_hi(wd[a]))
+                wd[a] = ld_relaxed_u64(xo + (size_t)cds[a] * S + s);
+          }
+          if (A.trace)
+            poll_cyc += clock64() - pc0;
+          double acc = __longlong_as_double((long long)rw);
+#pragma unroll
+          for (int a = 0; a < CHN; ++a)
+            if (a < m)
+              acc = __dsub_rn(acc, __dmul_rn(W.v[qv][b][a][s], __longlong_as_double((long long)wd[a])));
+          for (int e = e0 + CHN; e < e0 + nd; ++e) { // rows wider than the staging
+            const int cd = __ldg(code + e);
+            double xv;
+            if (cd >= 0) {
+              xv = poll_f64(xo + (size_t)cd * S + s, 0);
+            } else {
+              const int t = -1 - cd;
+              xv = W.ring[(i - (t >> 5)) & (kRing - 1)][(t & 31) * S + s];
+            }
+            acc = __dsub_rn(acc, __dmul_rn(__ldg(val + (size_t)e * S + s), xv));
+          }
+          if (chained)
+            acc = __dsub_rn(acc, __dmul_rn(W.v[qv][b][CHN][s], carry));
+          if (d == 0.0)
+            report_error(A.err, kern, bwd ? A.n - 1 - r : r, r);
+          const double xv = div_with_rcp(acc, d, rd);
+          publish_f64(xo + (size_t)r * S + s, xv);
+          W.ring[i & (kRing - 1)][lane] = xv;
+          carry = xv;
+        }
+      }
+      __syncwarp();
+    }
+    cp_wait0();
+    __syncwarp();
+    if (A.trace) {
+      unsigned long long pmax = poll_cyc;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const unsigned long long v = __shfl_xor_sync(FULL, pmax, o);
+        pmax = v > pmax ? v : pmax;
+      }
+      if (lane == 0) {
+        unsigned long long te;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(te));
+        unsigned long long* tr = A.trace + (size_t)item * 4;
+        tr[0] = tr_claim;
+        tr[1] = tr_first;
+        tr[2] = te;
+        tr[3] = (wait_cyc << 32) | (pmax & 0xffffffffull);
+      }
+    }
+  }
+}
+
+template <int S, int CHN> void launch_sc(const MLineArgs& a, cudaStream_t s) {
+  auto kern = k_mline<S, CHN>;
+  const size_t smem = (size_t)(kMThreads / 32) * sizeof(MlWarp<S, CHN>);
+  SFG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int per_sm = 0;
+  SFG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kMThreads, smem));
+  if (per_sm < 1)
+    per_sm = 1;
+  if (a.blocks_per_sm > 0 && a.blocks_per_sm < per_sm)
+    per_sm = a.blocks_per_sm;
+  const int64_t items = a.seg_end - a.seg_begin;
+  int64_t grid = (items + (kMThreads / 32) - 1) / (kMThreads / 32);
+  if (grid > (int64_t)per_sm * sm_count())
+    grid = (int64_t)per_sm * sm_count();
+  if (grid < 1)
+    return;
+  kern<<<(unsigned)grid, kMThreads, smem, s>>>(a);
+  count_launch();
+  SFG_CUDA(cudaGetLastError());
+}
+
+template <int S> void launch_s(const MLineArgs& a, cudaStream_t s) {
+  if (a.chn <= 4)
+    launch_sc<S, 4>(a, s);
+  else
+    launch_sc<S, 12>(a, s);
+}
+
+} // namespace
+
+void build_mline(const int32_t* ptr, const int32_t* idx, int32_t n, int dir, int32_t S,
+                 int32_t max_len, MLineLayout& out, cudaStream_t s) {
+  out.n = n;
+  out.S = S;
+  out.B = 32 / S;
+  out.dir = dir;
+  const int32_t B = out.B;
+  if (n == 0) {
+    out.nchain = out.ngroup = out.nlevels = 0;
+    out.cstart.alloc(1);
+    SFG_CUDA(cudaMemsetAsync(out.cstart.p, 0, sizeof(int32_t), s));
+    return;
+  }
+  // chains: maximal runs whose last dependency is the previous position
+  ChainLayout ch;
+  build_chains(ptr, idx, n, dir, 1, 1, max_len, ch, s);
+  out.nchain = ch.nchain;
+  out.cstart = std::move(ch.cstart);
+  const int32_t nc = out.nchain;
+  out.ngroup = (nc + B - 1) / B;
+  const int32_t ng = out.ngroup;
+  out.cskew.alloc(nc);
+  out.gsteps.alloc(ng);
+  SFG_CUDA(cudaMemsetAsync(out.cskew.p, 0, sizeof(int32_t) * (size_t)nc, s));
+  group_skew_kernel<<<mgrid(ng, 64), 64, 0, s>>>(ptr, idx, n, dir, out.cstart.p, ch.chain_of.p, nc,
+                                                  B, ng, out.cskew.p, out.gsteps.p);
+  count_launch();
+  SFG_CUDA(cudaGetLastError());
+  int32_t nnz = 0;
+  SFG_CUDA(cudaMemcpyAsync(&nnz, ptr + n, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+  SFG_CUDA(cudaStreamSynchronize(s));
+  out.code.alloc(nnz > 0 ? nnz : 1);
+  DBuf<uint64_t> keys(nnz > 0 ? nnz : 1);
+  DBuf<int> width(1);
+  SFG_CUDA(cudaMemsetAsync(width.p, 0, sizeof(int), s));
+  codes_kernel<<<mgrid(n), 256, 0, s>>>(ptr, idx, n, dir, out.cstart.p, ch.chain_of.p,
+                                         out.cskew.p, B, out.code.p, keys.p, width.p);
+  count_launch();
+  SFG_CUDA(cudaGetLastError());
+  SFG_CUDA(cudaMemcpyAsync(&out.CHN, width.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+  // group DAG -> levels -> claim order
+  DevDag gd;
+  csr_from_edge_keys(keys, nnz, ng, gd, s);
+  DBuf<int32_t> level(ng);
+  out.nlevels = levels_syncfree(gd.ptr.p, gd.idx.p, ng, +1, level.p, s);
+  out.gorder.alloc(ng);
+  order_by_level(level.p, ng, out.nlevels, out.gorder.p, nullptr, s);
+  // longest group (diagnostics)
+  std::vector<int32_t> hs((size_t)ng);
+  SFG_CUDA(cudaMemcpyAsync(hs.data(), out.gsteps.p, sizeof(int32_t) * (size_t)ng,
+                           cudaMemcpyDeviceToHost, s));
+  SFG_CUDA(cudaStreamSynchronize(s));
+  out.max_steps = 0;
+  for (int32_t v : hs)
+    out.max_steps = v > out.max_steps ? v : out.max_steps;
+}
+
+void launch_mline(const MLineArgs& a, cudaStream_t s) {
+  if (a.seg_end <= a.seg_begin)
+    return;
+  switch (a.S) {
+  case 1:
+    launch_s<1>(a, s);
+    break;
+  case 2:
+    launch_s<2>(a, s);
+    break;
+  case 4:
+    launch_s<4>(a, s);
+    break;
+  case 8:
+    launch_s<8>(a, s);
+    break;
+  case 16:
+    launch_s<16>(a, s);
+    break;
+  case 32:
+    launch_s<32>(a, s);
+    break;
+  default:
+    throw InvalidArgument("nsys must be a power of two <= 32");
+  }
+}
+
+} // namespace sfg

@@ -6,6 +6,7 @@
 #include "chain.cuh"
 #include "ell.cuh"
 #include "fact.cuh"
+#include "mline.cuh"
 #include "common.cuh"
 #include "executor.cuh"
 #include "internal.hpp"
@@ -74,6 +75,9 @@ struct sfg_plan {
   std::vector<int32_t> row_maxcol; // (unused by the chain path; kept for stats)
   int32_t tile_rows = 0;           // chain tile height override (S == 1)
   DBuf<unsigned long long> trace;  // SFG_TRACE diagnostics
+  // multi-chain warp executor (combos 1, 8; default)
+  bool use_mline = false;
+  MLineLayout ml_f, ml_b;
   // warp-per-task factorization executors (combos 5, 6, 7)
   bool use_warpfac = false;
   UpdateLists upd;
@@ -636,8 +640,30 @@ void do_inspect(sfg_plan* P) {
   }
   const char* ex = getenv("SFG_EXECUTOR");
   const bool legacy = ex && std::string(ex) == "levels";
-  if (combo == 1 || combo == 4 || combo == 8)
+  const bool want_mline = ex && std::string(ex) == "mline";
+  if (want_mline && (combo == 1 || combo == 8)) {
+    int32_t max_len = 1 << 20;
+    if (const char* e = getenv("SFG_CHAIN_MAX"))
+      max_len = atoi(e);
+    build_mline(P->lr_ptr.p, P->lr_idx.p, n, +1, P->nsys, max_len, P->ml_f, s);
+    if (combo == 8)
+      build_mline(P->lt_ptr.p, P->lt_idx.p, n, -1, P->nsys, max_len, P->ml_b, s);
+    P->use_mline = true;
+    if (getenv("SFG_MLINE_STATS")) {
+      for (const MLineLayout* L : {&P->ml_f, &P->ml_b})
+        if (L->nchain > 0)
+          fprintf(stderr, "mline dir=%d nchain=%d ngroup=%d levels=%d max_steps=%d width=%d\n",
+                  L->dir, L->nchain, L->ngroup, L->nlevels, L->max_steps, L->CHN);
+    }
+    if (getenv("SFG_TRACE")) {
+      P->trace_tiles = 4;
+      const int64_t items = (int64_t)P->ml_f.ngroup + (combo == 8 ? P->ml_b.ngroup : P->ml_f.ngroup);
+      P->trace.alloc(items * 4);
+      SFG_CUDA(cudaMemsetAsync(P->trace.p, 0, sizeof(unsigned long long) * items * 4, s));
+    }
+  } else if (combo == 1 || combo == 4 || combo == 8) {
     P->use_chain = !legacy;
+  }
   if (!legacy && (combo == 5 || combo == 7)) {
     build_ic0_updates(P->lc_ptr.p, P->lc_idx.p, P->rv_ptr.p, P->rv_col.p, P->rv_pos.p, n,
                       P->nnzF, P->upd, s);
@@ -710,6 +736,46 @@ EllArgs ell_args(sfg_plan* P) {
   a.vin = P->vin.p;
   a.vmid = P->vmid.p;
   a.vout = P->vout.p;
+  if (const char* e = getenv("SFG_BLOCKS_PER_SM"))
+    a.blocks_per_sm = atoi(e);
+  return a;
+}
+
+MLineArgs mline_args(sfg_plan* P) {
+  MLineArgs a;
+  a.combo = P->combo;
+  a.n = P->n;
+  a.S = P->nsys;
+  a.counter = P->counter.p;
+  a.err = P->err.p;
+  a.lr_ptr = P->lr_ptr.p;
+  a.lr_idx = P->lr_idx.p;
+  a.lr_val = P->lr_val.p;
+  a.f_cstart = P->ml_f.cstart.p;
+  a.f_cskew = P->ml_f.cskew.p;
+  a.f_gsteps = P->ml_f.gsteps.p;
+  a.f_gorder = P->ml_f.gorder.p;
+  a.f_code = P->ml_f.code.p;
+  a.f_nchain = P->ml_f.nchain;
+  a.f_ngroup = P->ml_f.ngroup;
+  const MLineLayout& L2 = P->combo == 8 ? P->ml_b : P->ml_f;
+  a.lt_ptr = P->combo == 8 ? P->lt_ptr.p : P->lr_ptr.p;
+  a.lt_idx = P->combo == 8 ? P->lt_idx.p : P->lr_idx.p;
+  a.lt_val = P->combo == 8 ? P->lt_val.p : P->lr_val.p;
+  a.b_cstart = L2.cstart.p;
+  a.b_cskew = L2.cskew.p;
+  a.b_gsteps = L2.gsteps.p;
+  a.b_gorder = L2.gorder.p;
+  a.b_code = L2.code.p;
+  a.b_nchain = L2.nchain;
+  a.b_ngroup = L2.ngroup;
+  a.vin = P->vin.p;
+  a.vmid = P->vmid.p;
+  a.vout = P->vout.p;
+  a.chn = std::max(P->ml_f.CHN, L2.CHN);
+  a.trace = P->trace.p;
+  if (const char* e = getenv("SFG_SLEEP_CAP"))
+    a.sleep_ns = (unsigned)atoi(e);
   if (const char* e = getenv("SFG_BLOCKS_PER_SM"))
     a.blocks_per_sm = atoi(e);
   return a;
@@ -1002,6 +1068,11 @@ void exec_fused_impl(sfg_plan* P, cudaEvent_t kb, cudaEvent_t ke) {
     e.seg_begin = 0;
     e.seg_end = P->ch_f.nbatch + P->ch_b.nbatch;
     launch_chain_ell(e, P->ell_chn, P->stream);
+  } else if (P->use_mline) {
+    MLineArgs m = mline_args(P);
+    m.seg_begin = 0;
+    m.seg_end = m.f_ngroup + m.b_ngroup;
+    launch_mline(m, P->stream);
   } else if (P->use_chain) {
     ChainArgs b = chain_args(P);
     b.phase = 3;
@@ -1043,6 +1114,19 @@ void exec_unfused_impl(sfg_plan* P, cudaEvent_t kb, cudaEvent_t ke) {
     e.seg_begin = P->ch_f.nbatch;
     e.seg_end = P->ch_f.nbatch + P->ch_b.nbatch;
     launch_chain_ell(e, P->ell_chn, P->stream);
+    SFG_CUDA(cudaEventRecord(ke, P->stream));
+    return;
+  }
+  if (P->use_mline) {
+    MLineArgs m = mline_args(P);
+    m.seg_begin = 0;
+    m.seg_end = m.f_ngroup;
+    launch_mline(m, P->stream);
+    FillRegion r2[1] = {{P->vout.p, nv}};
+    launch_prep(r2, 1, P->counter.p, nullptr, P->stream);
+    m.seg_begin = m.f_ngroup;
+    m.seg_end = m.f_ngroup + m.b_ngroup;
+    launch_mline(m, P->stream);
     SFG_CUDA(cudaEventRecord(ke, P->stream));
     return;
   }
@@ -1193,7 +1277,18 @@ sfg_status sfg_plan_destroy(sfg_plan* P) {
     DeviceScope ds(P->device);
     if (P->stream)
       cudaStreamSynchronize(P->stream);
-    if (P->trace.p) {
+    if (P->trace.p && P->use_mline) {
+      // SFG_TRACE=<path>: {items, 4, fwd items, data[items*4]} (see MLineArgs::trace)
+      const int64_t items = (int64_t)P->ml_f.ngroup + (P->combo == 8 ? P->ml_b.ngroup : P->ml_f.ngroup);
+      std::vector<unsigned long long> h((size_t)(items * 4));
+      cudaMemcpy(h.data(), P->trace.p, sizeof(unsigned long long) * h.size(), cudaMemcpyDeviceToHost);
+      if (FILE* f = fopen(getenv("SFG_TRACE"), "wb")) {
+        const int64_t hdr[3] = {items, 4, P->ml_f.ngroup};
+        fwrite(hdr, sizeof(hdr), 1, f);
+        fwrite(h.data(), sizeof(unsigned long long), h.size(), f);
+        fclose(f);
+      }
+    } else if (P->trace.p) {
       // SFG_TRACE=<path>: binary dump {items, tiles, data[items*tiles*3]}
       const int64_t items = (int64_t)P->ch_f.nbatch + P->ch_b.nbatch;
       std::vector<unsigned long long> h((size_t)(items * P->trace_tiles * 3));
@@ -1466,6 +1561,53 @@ sfg_status sfg_get_schedule(sfg_plan* P, int64_t* nentries, uint8_t* tags, int32
     return SFG_ERR_INVALID_ARGUMENT;
   if (!P->inspected)
     return set_err(P, SFG_ERR_LOGIC, "sfg_inspect has not run");
+  if (P->use_mline) {
+    return guarded(P, [&] {
+      DeviceScope ds(P->device);
+      auto fetch = [](const DBuf<int32_t>& d, int64_t cnt) {
+        std::vector<int32_t> h((size_t)std::max<int64_t>(cnt, 0));
+        if (cnt > 0)
+          SFG_CUDA(cudaMemcpy(h.data(), d.p, sizeof(int32_t) * (size_t)cnt, cudaMemcpyDeviceToHost));
+        return h;
+      };
+      std::vector<uint8_t> tg;
+      std::vector<int32_t> it;
+      std::vector<int64_t> wp{0};
+      // groups in claim order; inside a group, rows in step order
+      auto emit = [&](const MLineLayout& L, uint8_t tag) {
+        const auto cs = fetch(L.cstart, (int64_t)L.nchain + 1);
+        const auto sk = fetch(L.cskew, L.nchain);
+        const auto go = fetch(L.gorder, L.ngroup);
+        const auto gs = fetch(L.gsteps, L.ngroup);
+        for (int32_t q = 0; q < L.ngroup; ++q) {
+          const int32_t g = go[(size_t)q];
+          const int32_t c0 = g * L.B, c1 = std::min(L.nchain, c0 + L.B);
+          for (int32_t st = 0; st < gs[(size_t)g]; ++st)
+            for (int32_t c = c0; c < c1; ++c) {
+              const int32_t o = st - sk[(size_t)c];
+              if (o >= 0 && o < cs[(size_t)c + 1] - cs[(size_t)c]) {
+                tg.push_back(tag);
+                it.push_back(cs[(size_t)c] + o); // position (combo 8: i' = n-1-row)
+              }
+            }
+          wp.push_back((int64_t)tg.size());
+        }
+      };
+      emit(P->ml_f, 1);
+      emit(P->combo == 8 ? P->ml_b : P->ml_f, 2);
+      if (nentries)
+        *nentries = (int64_t)tg.size();
+      if (nwaves)
+        *nwaves = (int32_t)wp.size() - 1;
+      if (wave_ptr)
+        std::copy(wp.begin(), wp.end(), wave_ptr);
+      if (tags)
+        std::copy(tg.begin(), tg.end(), tags);
+      if (iters)
+        std::copy(it.begin(), it.end(), iters);
+      return SFG_OK;
+    });
+  }
   if (P->use_chain) {
     return guarded(P, [&] {
       DeviceScope ds(P->device);

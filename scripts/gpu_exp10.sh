@@ -1,0 +1,8 @@
+mkdir -p gpurun_out
+run() {
+  envs="$1"; shift
+  timeout 300 env $envs python bench.py --steps 10 --warmup 3 --no-cpu-baseline --no-extras "$@" > /tmp/o.json 2>/tmp/e.txt
+  python -c "import json,sys;d=json.load(open('/tmp/o.json'));print('$envs $* ms=%.3f kernel=%.3f unfused=%.3f'%(d['ms_per_step'],d['roofline']['kernel_ms'],d['unfused']['ms_per_step']))" >> gpurun_out/exp10.txt 2>&1 || (echo "$envs $* FAILED" >> gpurun_out/exp10.txt; tail -3 /tmp/e.txt >> gpurun_out/exp10.txt)
+}
+for g in 1 2 4; do run "SFG_CHAIN_G=$g" --config 5; done
+for g in 1 2; do SFG_CHAIN_G=$g timeout 600 python -m pytest tests/test_gpu_parity.py -q -x -k "config5 or multisystem" -p no:cacheprovider >> gpurun_out/exp10.txt 2>&1; done

@@ -22,7 +22,7 @@ print("kernel ms", ker)
 st.close()
 raw = np.fromfile(out, dtype=np.int64)
 items, tiles, nf = raw[:3]
-d = raw[3:].view(np.uint64).reshape(items, tiles, 3).astype(np.float64)
+d = raw[3:3 + items * tiles * 3].view(np.uint64).reshape(items, tiles, 3).astype(np.float64)
 valid = d[:, :, 2] > 0
 t0 = d[valid][:, 0].min()
 d = (d - t0) / 1e3  # us

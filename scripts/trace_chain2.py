@@ -15,7 +15,7 @@ print("kernel ms", st.bench(1)[1])
 st.close()
 raw = np.fromfile(out, dtype=np.int64)
 items, tiles, nf = raw[:3]
-d = raw[3:].view(np.uint64).reshape(items, tiles, 3)
+d = raw[3:3 + items * tiles * 3].view(np.uint64).reshape(items, tiles, 3)
 valid = d[:, :, 2] > 0
 wait = (d[:, :, 1] >> 32).astype(np.float64)[valid]
 carry = (d[:, :, 1] & 0xffffffff).astype(np.float64)[valid]

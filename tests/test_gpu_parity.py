@@ -286,3 +286,36 @@ def test_set_values_zero_diagonal(golden, combo):
     v2[p] = 0.0
     with pytest.raises(sf.InvalidMatrixError, match="zero diagonal entry at column 4"):
         st.set_values(v2)
+
+
+# ---- alternative executors (SFG_EXECUTOR, read at sfg_inspect) -----------------
+@pytest.mark.parametrize("executor", ("levels", "mline"))
+@pytest.mark.parametrize("name", GOLDEN_MATS)
+def test_alternative_executors_golden(golden, monkeypatch, executor, name):
+    monkeypatch.setenv("SFG_EXECUTOR", executor)
+    M = as_sf(golden_matrix(golden, name))
+    for combo in (1, 8) if executor == "mline" else GPU_COMBOS:
+        st = sf.make_state(combo, M, seed=7).inspect()
+        st.execute_fused()
+        if combo == 8:
+            continue  # golden has no combo 8; covered against the oracle below
+        assert np.array_equal(st.collect_outputs(), golden[f"{name}/c{combo}/outputs"])
+        st.execute_unfused()
+        assert np.array_equal(st.collect_outputs(), golden[f"{name}/c{combo}/outputs"])
+        _check_linear_extension(st, st.dag(3))
+
+
+@pytest.mark.parametrize("nsys", (1, 2, 8, 32))
+def test_mline_executor_vs_oracle(orc, monkeypatch, nsys):
+    monkeypatch.setenv("SFG_EXECUTOR", "mline")
+    M, vals = sf.config5_systems(size=24, nsys=nsys)
+    n, nnz = M.n, M.nnz
+    vin = np.concatenate([sf.gen_vector(n, 7 + s) for s in range(nsys)])
+    for combo in (8, 1):
+        st = sf.make_state(combo, M, nsys=nsys, values=vals, vin=vin)
+        st.execute_fused()
+        got = st.collect_outputs().reshape(nsys, 2 * n)
+        for s in range(nsys):
+            Ms = Csc(n, M.colptr, M.rowidx, vals[s * nnz:(s + 1) * nnz])
+            want = orc.run_sequential(combo, Ms, 7, vin=vin[s * n:(s + 1) * n])
+            assert np.array_equal(got[s], want)
