@@ -11,10 +11,16 @@ namespace sfg {
 namespace {
 
 constexpr unsigned FULL = 0xffffffffu;
-constexpr int kMThreads = 128; // 4 warps per CTA
-constexpr int QC = 5;          // meta / code slots: steps i .. i+4
-constexpr int QV = 4;          // value / rhs slots: steps i .. i+3
-constexpr int QX = 3;          // gathered x slots: steps i .. i+2
+constexpr int kMThreads = 64; // 2 warps per CTA (several CTAs per SM as smem allows)
+
+// Pipeline distances, in steps, for a lookahead DX: external x words are
+// gathered DX steps ahead, values DV = DX+1, dependency codes DC = 2 DX and
+// row pointers DP = 3 DX ahead, so every operand a stage reads was copied by
+// a commit group at least DX iterations old (cp.async.wait_group DX-1).
+template <int DX> struct Dist {
+  static constexpr int DV = DX + 1, DC = 2 * DX, DP = 3 * DX;
+  static constexpr int QX = DX + 1, QV = DV + 1, QC = DC + 1, QP = DP - DC + 1;
+};
 
 inline unsigned mgrid(int64_t work, int block = 256) {
   int64_t g = (work + block - 1) / block;
@@ -114,34 +120,43 @@ __global__ void codes_kernel(const int32_t* __restrict__ ptr, const int32_t* __r
 // executor
 // ---------------------------------------------------------------------------
 
-template <int S, int CHN> struct MlWarp {
+template <int S, int CHN, int DX> struct MlWarp {
   static constexpr int B = 32 / S;
-  int32_t code[QC][B][CHN];
-  int32_t meta[QC][B][4]; // row (-1 = idle), first dependency entry, #deps, chained
-  int32_t rptr[3][B][2];  // row pointers of steps i+4 .. i+6
-  double v[QV][B][CHN + 2][S]; // deps, carry coefficient, diagonal
-  unsigned long long x[QX][B][CHN][S];
-  unsigned long long rhs[QV][B][S];
+  using D = Dist<DX>;
+  int32_t code[D::QC][B][CHN];
+  int32_t meta[D::QC][B][4]; // row (-1 = idle), first dependency entry, #deps, chained
+  int32_t rptr[D::QP][B][2];
+  double v[D::QV][B][CHN + 2][S]; // deps, carry coefficient, diagonal
+  unsigned long long x[D::QX][B][CHN][S];
+  unsigned long long rhs[D::QV][B][S];
   double ring[kRing][32];
 };
 
 __device__ __forceinline__ void cp8(void* dst, const void* src) {
   const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(src) : "memory");
+  // no "memory" clobber: the copy's destination is only read after a
+  // cp.async.wait_group (which has one), so the compiler may interleave the
+  // stages' independent shared-memory loads with the copy issue
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(src));
 }
 __device__ __forceinline__ void cp4(void* dst, const void* src) {
   const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(d), "l"(src) : "memory");
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(d), "l"(src));
 }
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void cp_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+template <int N> __device__ __forceinline__ void cp_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
 __device__ __forceinline__ void cp_wait0() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
-template <int S, int CHN>
+template <int S, int CHN, int DX>
 __global__ void __launch_bounds__(kMThreads) k_mline(const MLineArgs A) {
   constexpr int B = 32 / S;
+  using D = Dist<DX>;
+  constexpr int DV = D::DV, DC = D::DC, DP = D::DP;
+  constexpr int QX = D::QX, QV = D::QV, QC = D::QC, QP = D::QP;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  MlWarp<S, CHN>& W = reinterpret_cast<MlWarp<S, CHN>*>(smem_raw)[threadIdx.x >> 5];
+  MlWarp<S, CHN, DX>& W = reinterpret_cast<MlWarp<S, CHN, DX>*>(smem_raw)[threadIdx.x >> 5];
   const int lane = threadIdx.x & 31;
   const int b = lane / S;
   const int s = lane % S;
@@ -154,6 +169,64 @@ __global__ void __launch_bounds__(kMThreads) k_mline(const MLineArgs A) {
     if (wi >= total)
       break;
     const int item = A.seg_begin + (int)wi;
+    if (S == 1 && A.combo == 4 && item >= A.f_ngroup) {
+      // combo 4 kernel 2: SpMV rows (item - f_ngroup) * 32 + lane as a row
+      // gather over CSR(A) in ascending column order -- the order in which
+      // the sequential CSC scatter (spmv_csc_col, kernels.hpp:162-168)
+      // accumulates y_r, so the sum is the reference's bit for bit.
+      const int r = (item - A.f_ngroup) * 32 + lane;
+      {
+        // one lane watches the block's newest operand (the last row's
+        // largest column) with a long back-off before the block gathers
+        const int rl = min((item - A.f_ngroup) * 32 + 31, A.n - 1);
+        if (lane == 0) {
+          const int pl = __ldg(A.ar_ptr + rl + 1) - 1;
+          if (pl >= 0) {
+            const int jl = __ldg(A.ar_idx + pl);
+            while (is_sent_hi(ld_relaxed_u64(A.vmid + jl)))
+              __nanosleep(1000);
+          }
+        }
+        __syncwarp();
+      }
+      if (r < A.n) {
+        const int pb = __ldg(A.ar_ptr + r), pe = __ldg(A.ar_ptr + r + 1);
+        double acc = 0.0;
+        for (int p = pb; p < pe; p += 8) {
+          const int cnt = pe - p < 8 ? pe - p : 8;
+          int jj[8];
+          unsigned long long ww[8];
+#pragma unroll
+          for (int a = 0; a < 8; ++a)
+            if (a < cnt)
+              jj[a] = __ldg(A.ar_idx + p + a);
+          // wait for the whole batch with a long back-off: these warps have
+          // nothing else to do and must not steal L2 bandwidth or issue
+          // slots from the solve they wait on
+          for (bool first = true;; first = false) {
+            bool pending = false;
+#pragma unroll
+            for (int a = 0; a < 8; ++a)
+              if (a < cnt && (first || is_sent_hi(ww[a]))) {
+                ww[a] = ld_relaxed_u64(A.vmid + jj[a]);
+              }
+#pragma unroll
+            for (int a = 0; a < 8; ++a)
+              pending |= a < cnt && is_sent_hi(ww[a]);
+            if (!pending)
+              break;
+            __nanosleep(1000);
+          }
+#pragma unroll
+          for (int a = 0; a < 8; ++a)
+            if (a < cnt)
+              acc = __dadd_rn(acc, __dmul_rn(__ldg(A.ar_val + p + a),
+                                             __longlong_as_double((long long)ww[a])));
+        }
+        A.vout[r] = acc;
+      }
+      continue;
+    }
     const bool second = item >= A.f_ngroup;
     const bool bwd = second && A.combo == 8;
     const int32_t* ptr = bwd ? A.lt_ptr : A.lr_ptr;
@@ -187,34 +260,34 @@ __global__ void __launch_bounds__(kMThreads) k_mline(const MLineArgs A) {
     // iterations in a register (a register hand-off would stall the warp on
     // the load at the end of every step).
 #pragma unroll 1
-    for (int i = -6; i < T; ++i) {
+    for (int i = -DP; i < T; ++i) {
       if (A.trace && i == 0)
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tr_first));
-      // groups <= i-2 complete: row pointers of step i+4, codes of step i+2,
-      // values of step i+1 and gathered x of step i
+      // commit groups <= i-DX complete: row pointers of step i+DC, codes of
+      // step i+DX, values and gathered x of step i
       const long long wc0 = A.trace ? clock64() : 0;
-      cp_wait1();
+      cp_wait<DX - 1>();
       __syncwarp();
       if (A.trace)
         wait_cyc += clock64() - wc0;
-      // ---- stage A: row pointers of step i+6
-      {
-        const int o = i + 6 - skew;
+      // ---- stage A: row pointers of step i+DP
+      if (i + DP >= 0) {
+        const int o = i + DP - skew;
         if (s == 0 && o >= 0 && o < len) {
           const int r = row_of(o);
-          cp4(&W.rptr[(i + 6) % 3][b][0], ptr + r);
-          cp4(&W.rptr[(i + 6) % 3][b][1], ptr + r + 1);
+          cp4(&W.rptr[(i + DP) % QP][b][0], ptr + r);
+          cp4(&W.rptr[(i + DP) % QP][b][1], ptr + r + 1);
         }
       }
-      // ---- stage B': meta + dependency codes of step i+4
-      if (i + 4 >= 0) {
-        const int q = (i + 4) % QC;
-        const int o = i + 4 - skew;
+      // ---- stage B': meta + dependency codes of step i+DC
+      if (i + DC >= 0) {
+        const int q = (i + DC) % QC;
+        const int o = i + DC - skew;
         const bool act = o >= 0 && o < len;
         const bool chained = o > 0;
         const int r = act ? row_of(o) : -1;
-        const int e0 = act ? W.rptr[(i + 4) % 3][b][0] : 0;
-        const int e1 = act ? W.rptr[(i + 4) % 3][b][1] : 0;
+        const int e0 = act ? W.rptr[(i + DC) % QP][b][0] : 0;
+        const int e1 = act ? W.rptr[(i + DC) % QP][b][1] : 0;
         const int nd = act ? e1 - e0 - 1 - (chained ? 1 : 0) : 0;
         if (s == 0) {
           W.meta[q][b][0] = r;
@@ -229,10 +302,10 @@ __global__ void __launch_bounds__(kMThreads) k_mline(const MLineArgs A) {
         }
       }
       __syncwarp();
-      // ---- stage B: values and right-hand side of step i+3
-      if (i + 3 >= 0) {
-        const int q = (i + 3) % QC;
-        const int qv = (i + 3) % QV;
+      // ---- stage B: values and right-hand side of step i+DV
+      if (i + DV >= 0) {
+        const int q = (i + DV) % QC;
+        const int qv = (i + DV) % QV;
         const int r = W.meta[q][b][0];
         if (r >= 0) {
           const int e0 = W.meta[q][b][1];
@@ -251,10 +324,10 @@ __global__ void __launch_bounds__(kMThreads) k_mline(const MLineArgs A) {
           cp8(&W.rhs[qv][b][s], rhs_vec + (size_t)r * S + s);
         }
       }
-      // ---- stage C: gather the external x words of step i+2
-      if (i + 2 >= 0) {
-        const int q = (i + 2) % QC;
-        const int qx = (i + 2) % QX;
+      // ---- stage C: gather the external x words of step i+DX
+      if (i + DX >= 0) {
+        const int q = (i + DX) % QC;
+        const int qx = (i + DX) % QX;
         if (W.meta[q][b][0] >= 0) {
           const int nd = W.meta[q][b][2];
           const int m = nd < CHN ? nd : CHN;
@@ -367,9 +440,11 @@ __global__ void __launch_bounds__(kMThreads) k_mline(const MLineArgs A) {
   }
 }
 
-template <int S, int CHN> void launch_sc(const MLineArgs& a, cudaStream_t s) {
-  auto kern = k_mline<S, CHN>;
-  const size_t smem = (size_t)(kMThreads / 32) * sizeof(MlWarp<S, CHN>);
+template <int S, int CHN, int DX> void launch_scd(const MLineArgs& a, cudaStream_t s) {
+  // single-system plans are latency-bound: one CTA per SM keeps the solve
+  // warps from sharing schedulers with waiting warps (measured on C1)
+  auto kern = k_mline<S, CHN, DX>;
+  const size_t smem = (size_t)(kMThreads / 32) * sizeof(MlWarp<S, CHN, DX>);
   SFG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int per_sm = 0;
   SFG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kMThreads, smem));
@@ -377,6 +452,8 @@ template <int S, int CHN> void launch_sc(const MLineArgs& a, cudaStream_t s) {
     per_sm = 1;
   if (a.blocks_per_sm > 0 && a.blocks_per_sm < per_sm)
     per_sm = a.blocks_per_sm;
+  else if (a.blocks_per_sm == 0 && S == 1)
+    per_sm = 1;
   const int64_t items = a.seg_end - a.seg_begin;
   int64_t grid = (items + (kMThreads / 32) - 1) / (kMThreads / 32);
   if (grid > (int64_t)per_sm * sm_count())
@@ -386,6 +463,13 @@ template <int S, int CHN> void launch_sc(const MLineArgs& a, cudaStream_t s) {
   kern<<<(unsigned)grid, kMThreads, smem, s>>>(a);
   count_launch();
   SFG_CUDA(cudaGetLastError());
+}
+
+template <int S, int CHN> void launch_sc(const MLineArgs& a, cudaStream_t s) {
+  if (a.lookahead <= 2)
+    launch_scd<S, CHN, 2>(a, s);
+  else
+    launch_scd<S, CHN, 4>(a, s);
 }
 
 template <int S> void launch_s(const MLineArgs& a, cudaStream_t s) {

@@ -1,4 +1,4 @@
-// mline.cuh -- multi-chain warp executor for the solve pairs (combos 1, 8).
+// mline.cuh -- multi-chain warp executor for the solve pairs (combos 1, 4, 8).
 //
 // A warp owns a GROUP of B = 32/S consecutive chains (chain = maximal run of
 // positions whose last dependency is the previous position, see chain.cuh)
@@ -68,11 +68,15 @@ struct MLineArgs {
   const int32_t *b_cstart = nullptr, *b_cskew = nullptr, *b_gsteps = nullptr,
                 *b_gorder = nullptr, *b_code = nullptr;
   int32_t b_nchain = 0, b_ngroup = 0;
+  // combo 4: CSR(A) for the SpMV row blocks (b_ngroup = number of blocks)
+  const int32_t *ar_ptr = nullptr, *ar_idx = nullptr;
+  const double* ar_val = nullptr;
   const double* vin = nullptr;
   double* vmid = nullptr;
   double* vout = nullptr;
   int blocks_per_sm = 0;
   unsigned sleep_ns = 0; // back-off between re-polls of unpublished words
+  int lookahead = 4;     // pipeline distance of the x gathers (2 or 4 steps)
   int32_t chn = 12; // staging width the kernel is instantiated for
   // diagnostics (SFG_TRACE): per work item {claim ns, first step ns, end ns,
   // stall cycles in cp.async waits << 32 | cycles in re-polls}

@@ -640,8 +640,11 @@ void do_inspect(sfg_plan* P) {
   }
   const char* ex = getenv("SFG_EXECUTOR");
   const bool legacy = ex && std::string(ex) == "levels";
-  const bool want_mline = ex && std::string(ex) == "mline";
-  if (want_mline && (combo == 1 || combo == 8)) {
+  // executor choice: the multi-chain warp executor for single-system solve
+  // pairs (latency-bound: in-warp dependencies go through shared memory),
+  // the chain executor for batched systems; SFG_EXECUTOR overrides
+  const bool want_mline = ex ? std::string(ex) == "mline" : P->nsys == 1;
+  if (want_mline && (combo == 1 || combo == 4 || combo == 8)) {
     int32_t max_len = 1 << 20;
     if (const char* e = getenv("SFG_CHAIN_MAX"))
       max_len = atoi(e);
@@ -759,6 +762,9 @@ MLineArgs mline_args(sfg_plan* P) {
   a.f_nchain = P->ml_f.nchain;
   a.f_ngroup = P->ml_f.ngroup;
   const MLineLayout& L2 = P->combo == 8 ? P->ml_b : P->ml_f;
+  a.ar_ptr = P->ar_ptr.p;
+  a.ar_idx = P->ar_idx.p;
+  a.ar_val = P->ar_val.p;
   a.lt_ptr = P->combo == 8 ? P->lt_ptr.p : P->lr_ptr.p;
   a.lt_idx = P->combo == 8 ? P->lt_idx.p : P->lr_idx.p;
   a.lt_val = P->combo == 8 ? P->lt_val.p : P->lr_val.p;
@@ -768,7 +774,7 @@ MLineArgs mline_args(sfg_plan* P) {
   a.b_gorder = L2.gorder.p;
   a.b_code = L2.code.p;
   a.b_nchain = L2.nchain;
-  a.b_ngroup = L2.ngroup;
+  a.b_ngroup = P->combo == 4 ? (P->n + 31) / 32 : L2.ngroup;
   a.vin = P->vin.p;
   a.vmid = P->vmid.p;
   a.vout = P->vout.p;
@@ -776,6 +782,8 @@ MLineArgs mline_args(sfg_plan* P) {
   a.trace = P->trace.p;
   if (const char* e = getenv("SFG_SLEEP_CAP"))
     a.sleep_ns = (unsigned)atoi(e);
+  if (const char* e = getenv("SFG_MLINE_DX"))
+    a.lookahead = atoi(e);
   if (const char* e = getenv("SFG_BLOCKS_PER_SM"))
     a.blocks_per_sm = atoi(e);
   return a;
@@ -1594,7 +1602,16 @@ sfg_status sfg_get_schedule(sfg_plan* P, int64_t* nentries, uint8_t* tags, int32
         }
       };
       emit(P->ml_f, 1);
-      emit(P->combo == 8 ? P->ml_b : P->ml_f, 2);
+      if (P->combo == 4) { // SpMV rows after every forward row
+        for (int32_t r = 0; r < P->n; ++r) {
+          tg.push_back(2);
+          it.push_back(r);
+          if ((r & 31) == 31 || r == P->n - 1)
+            wp.push_back((int64_t)tg.size());
+        }
+      } else {
+        emit(P->combo == 8 ? P->ml_b : P->ml_f, 2);
+      }
       if (nentries)
         *nentries = (int64_t)tg.size();
       if (nwaves)
