@@ -16,6 +16,9 @@
  *
  * Combos (kernels.hpp:53-68):
  *   1 sptrsv-sptrsv  x = inv(L)*b; z = inv(L)*x      (nsys >= 1)
+ *   2 spmv-sptrsv    y = A*b; z = inv(L)*y
+ *   3 dscal-spilu0   LU ~= D*A*D'  (make_state fails with SFG_ERR_FACTORIZATION,
+ *                    "zero diagonal", on a zero or missing diagonal)
  *   4 sptrsv-spmv    y = inv(L)*b; z = A*y
  *   5 spic0-sptrsv   L*L' ~= A; y = inv(L)*b
  *   6 spilu0-sptrsv  LU ~= A; y = inv(L)*b  (unit L)

@@ -237,6 +237,8 @@ inline KernelState make_state(int combo_id, const CscMatrix& M, std::uint64_t se
     if (p)
       sfg_plan_destroy(p);
     const std::string m = msg.empty() ? std::string("make_state") : msg;
+    if (s == SFG_ERR_FACTORIZATION) // combo 3's scaling_vector (kernels.hpp:299-309)
+      throw FactorizationError(m, index);
     if (s == SFG_ERR_INVALID_MATRIX)
       throw InvalidMatrixError(m);
     if (s == SFG_ERR_INVALID_ARGUMENT)

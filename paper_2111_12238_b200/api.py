@@ -29,6 +29,8 @@ from .abi import f64p, i32p, i64p, ptr, u8p
 # kernels.hpp:53-68 plus combo 8 (forward L, backward L^T; BASELINE config 5)
 COMBOS = {
     1: ("sptrsv-sptrsv", "x = inv(L)*y; z = inv(L)*x"),
+    2: ("spmv-sptrsv", "y = A*x; z = inv(L)*y"),
+    3: ("dscal-spilu0", "LU ~= D*A*D'"),
     4: ("sptrsv-spmv", "y = inv(L)*x; z = A*y"),
     5: ("spic0-sptrsv", "L*L' ~= A; y = inv(L)*x"),
     6: ("spilu0-sptrsv", "LU ~= A; y = inv(L)*x"),

@@ -269,11 +269,17 @@ __global__ void __launch_bounds__(kBlock) k_ic0(const ExecArgs A) {
 // solve (trsv_csr_unit_row, kernels.hpp:184-196): the solve's l_ik are the
 // multipliers the factorization just produced, still in registers.
 // ---------------------------------------------------------------------------
+// COMBO 3 (DSCAL -> ILU0, kernels.hpp:274-279 then 246-272): the row is
+// scaled on load, (d_i * a_ij) * d_j, when fused, or read from `work` after a
+// separate DSCAL launch; there is no solve.
+template <int COMBO>
 __global__ void __launch_bounds__(kBlock) k_ilu0(const ExecArgs A) {
   const int lane = threadIdx.x & 31;
   const int64_t total = A.t_end - A.t_begin;
-  const bool do_fac = A.phase & 1;
-  const bool do_solve = A.phase & 2;
+  const bool do_fac = COMBO == 6 ? (A.phase & 1) : (A.phase & 2);
+  const bool do_solve = COMBO == 6 && (A.phase & 2);
+  const int src = COMBO == 6 ? 0 : ((A.phase & 1) ? 1 : 2);
+  const int fac_kernel = COMBO == 6 ? 1 : 2;
   double accl[MAXC];
   int coll[MAXC];
   for (;;) {
@@ -291,10 +297,14 @@ __global__ void __launch_bounds__(kBlock) k_ilu0(const ExecArgs A) {
     if (do_fac) {
       const bool local = m <= MAXC;
       double* acc = local ? accl : A.work + r0;
+      const double di = src == 1 ? __ldg(A.dvec + i) : 0.0;
       for (int a = 0; a < m; ++a) {
+        const int cj = __ldg(A.ar_idx + r0 + a);
         if (local)
-          coll[a] = __ldg(A.ar_idx + r0 + a);
-        acc[a] = __ldg(A.ar_val + r0 + a);
+          coll[a] = cj;
+        acc[a] = src == 0   ? __ldg(A.ar_val + r0 + a)
+                 : src == 1 ? __dmul_rn(__dmul_rn(di, __ldg(A.ar_val + r0 + a)), __ldg(A.dvec + cj))
+                            : A.work[r0 + a];
       }
 #define COL(a) (local ? coll[(a)] : __ldg(A.ar_idx + r0 + (a)))
       for (int a = 0; a < m; ++a) {
@@ -304,7 +314,7 @@ __global__ void __launch_bounds__(kBlock) k_ilu0(const ExecArgs A) {
         const int dk = __ldg(A.diag + k);
         const double piv = dk >= 0 ? poll_f64(A.fac + dk, A.sleep_cap) : 0.0;
         if (dk < 0 || piv == 0.0)
-          report_error(A.err, 1, i, k);
+          report_error(A.err, fac_kernel, i, k);
         const double lik = __ddiv_rn(acc[a], piv);
         acc[a] = lik;
         if (dk >= 0) {
@@ -336,6 +346,17 @@ __global__ void __launch_bounds__(kBlock) k_ilu0(const ExecArgs A) {
     }
     if (do_solve)
       publish_f64(A.vout + i, acc2);
+  }
+}
+
+// DSCAL over CSR rows alone (combo 3 kernel 1 in the unfused comparator):
+// work[p] = (d_i * a_p) * d_j (dscal_csr_row, kernels.hpp:274-279).
+__global__ void __launch_bounds__(kBlock) k_dscal_csr(const ExecArgs A) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < A.n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const double di = __ldg(A.dvec + i);
+    for (int p = __ldg(A.ar_ptr + i); p < __ldg(A.ar_ptr + i + 1); ++p)
+      A.work[p] = __dmul_rn(__dmul_rn(di, __ldg(A.ar_val + p)), __ldg(A.dvec + __ldg(A.ar_idx + p)));
   }
 }
 
@@ -471,8 +492,23 @@ void launch_ic0(int combo, const ExecArgs& a, cudaStream_t s) {
     launch_persistent(k_ic0<7>, a, s, 32);
 }
 
-void launch_ilu0(const ExecArgs& a, cudaStream_t s) {
-  launch_persistent(k_ilu0, a, s, 32);
+void launch_ilu0(int combo, const ExecArgs& a, cudaStream_t s) {
+  if (combo == 3)
+    launch_persistent(k_ilu0<3>, a, s, 32);
+  else
+    launch_persistent(k_ilu0<6>, a, s, 32);
+}
+
+void launch_dscal_csr(const ExecArgs& a, cudaStream_t s) {
+  int64_t blocks = ((int64_t)a.n + kBlock - 1) / kBlock;
+  const int64_t cap = (int64_t)sm_count() * 8;
+  if (blocks > cap)
+    blocks = cap;
+  if (blocks < 1)
+    blocks = 1;
+  k_dscal_csr<<<(unsigned)blocks, kBlock, 0, s>>>(a);
+  count_launch();
+  SFG_CUDA(cudaGetLastError());
 }
 
 void launch_dscal(const ExecArgs& a, cudaStream_t s) {

@@ -64,8 +64,10 @@ void launch_prep(const FillRegion* regions, int nregions,
 void launch_trsv_pair(int combo, const ExecArgs& a, cudaStream_t s);
 // combo in {5, 7}
 void launch_ic0(int combo, const ExecArgs& a, cudaStream_t s);
-// combo 6
-void launch_ilu0(const ExecArgs& a, cudaStream_t s);
+// combo in {3, 6}
+void launch_ilu0(int combo, const ExecArgs& a, cudaStream_t s);
+// combo 3 kernel 1 alone (unfused): work[p] = (d_i * a_p) * d_j over CSR rows
+void launch_dscal_csr(const ExecArgs& a, cudaStream_t s);
 // combo 7 kernel 1 alone (unfused): work[p] = (d_i * a_p) * d_j
 void launch_dscal(const ExecArgs& a, cudaStream_t s);
 

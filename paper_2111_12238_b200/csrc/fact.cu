@@ -280,14 +280,20 @@ __global__ void __launch_bounds__(kFBlock) k_ic0_warp(const ExecArgs A,
 // once the updates of steps < t have reached it, the multiplier is broadcast,
 // and every lane holding a matching U(k_t, j) applies it.  The reciprocals of
 // all pivots are formed before the first step, off the serial chain.
+// COMBO 3 (DSCAL -> ILU0): no solve; the row is scaled on load,
+// (d_i * a_ij) * d_j (dscal_csr_row, kernels.hpp:274-279), when fused, or
+// read from `work` after a separate DSCAL launch.
+template <int COMBO>
 __global__ void __launch_bounds__(kFBlock) k_ilu0_warp(const ExecArgs A,
                                                        const int32_t* __restrict__ uptr,
                                                        const int32_t* __restrict__ ustep,
                                                        const int32_t* __restrict__ usrc) {
   const int lane = threadIdx.x & 31;
   const int64_t total = A.t_end - A.t_begin;
-  const bool do_fac = A.phase & 1;
-  const bool do_solve = A.phase & 2;
+  const bool do_fac = COMBO == 6 ? (A.phase & 1) : (A.phase & 2);
+  const bool do_solve = COMBO == 6 && (A.phase & 2);
+  const int src = COMBO == 6 ? 0 : ((A.phase & 1) ? 1 : 2);
+  const int fac_kernel = COMBO == 6 ? 1 : 2;
   const unsigned cap = A.sleep_cap;
   for (;;) {
     const long long c = claim_tickets(A.counter, 1);
@@ -305,7 +311,12 @@ __global__ void __launch_bounds__(kFBlock) k_ilu0_warp(const ExecArgs A,
       wx = ld_relaxed_u64(A.vout + col);
     double acc2 = do_solve ? __ldg(A.vin + i) : 0.0;
     if (do_fac) {
-      double acc = lane < m ? __ldg(A.ar_val + pb) : 0.0;
+      double acc = 0.0;
+      if (lane < m)
+        acc = src == 0   ? __ldg(A.ar_val + pb)
+              : src == 1 ? __dmul_rn(__dmul_rn(__ldg(A.dvec + i), __ldg(A.ar_val + pb)),
+                                     __ldg(A.dvec + col))
+                         : __ldg(A.work + pb);
       const int dk = lower ? __ldg(A.diag + col) : -1;
       unsigned long long wp = 0;
       if (dk >= 0)
@@ -340,7 +351,7 @@ __global__ void __launch_bounds__(kFBlock) k_ilu0_warp(const ExecArgs A,
       for (int t = 0; t < nl; ++t) {
         if (lane == t) {
           if (dk < 0 || piv == 0.0)
-            report_error(A.err, 1, i, col);
+            report_error(A.err, fac_kernel, i, col);
           acc = div_with_rcp(acc, piv, rcp);
         }
         const double lik = __shfl_sync(FULL, acc, t);
@@ -434,8 +445,11 @@ void launch_ic0_warp(int combo, const ExecArgs& a, const UpdateLists& up, cudaSt
     launch_warp_tasks(k_ic0_warp<7>, a, up, s);
 }
 
-void launch_ilu0_warp(const ExecArgs& a, const UpdateLists& up, cudaStream_t s) {
-  launch_warp_tasks(k_ilu0_warp, a, up, s);
+void launch_ilu0_warp(int combo, const ExecArgs& a, const UpdateLists& up, cudaStream_t s) {
+  if (combo == 3)
+    launch_warp_tasks(k_ilu0_warp<3>, a, up, s);
+  else
+    launch_warp_tasks(k_ilu0_warp<6>, a, up, s);
 }
 
 } // namespace sfg

@@ -38,7 +38,7 @@ struct UpdateLists {
 void build_ic0_updates(const int32_t* lc_ptr, const int32_t* lc_idx, const int32_t* rv_ptr,
                        const int32_t* rv_col, const int32_t* rv_pos, int32_t n, int64_t nnz,
                        UpdateLists& out, cudaStream_t s);
-// combo 6: A in CSR (ar_*) with diagonal positions
+// combos 3, 6: A in CSR (ar_*) with diagonal positions
 void build_ilu0_updates(const int32_t* ar_ptr, const int32_t* ar_idx, const int32_t* diag,
                         int32_t n, int64_t nnz, UpdateLists& out, cudaStream_t s);
 
@@ -50,6 +50,6 @@ bool ilu0_warp_fits(const UpdateLists& up);
 // Launches for one ticket range (ExecArgs as for the thread-per-task
 // kernels); up = the update lists.
 void launch_ic0_warp(int combo, const ExecArgs& a, const UpdateLists& up, cudaStream_t s);
-void launch_ilu0_warp(const ExecArgs& a, const UpdateLists& up, cudaStream_t s);
+void launch_ilu0_warp(int combo, const ExecArgs& a, const UpdateLists& up, cudaStream_t s);
 
 } // namespace sfg

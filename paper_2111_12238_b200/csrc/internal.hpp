@@ -21,6 +21,13 @@ struct InvalidMatrix : std::runtime_error {
 struct InvalidArgument : std::runtime_error {
   using std::runtime_error::runtime_error;
 };
+// A factorization error detected while building a plan (scaling_vector's
+// "zero diagonal", kernels.hpp:299-309, thrown by make_state for combo 3).
+struct FactorizationFailure : std::runtime_error {
+  int32_t kind, index;
+  FactorizationFailure(const std::string& w, int32_t k, int32_t i)
+      : std::runtime_error(w), kind(k), index(i) {}
+};
 
 void cuda_check(cudaError_t e, const char* what);
 #define SFG_CUDA(x) ::sfg::cuda_check((x), #x)
@@ -104,6 +111,11 @@ void find_diag_positions(const int32_t* rowptr, const int32_t* colidx,
 
 // d[j] = 1 / sqrt(|L_jj|) with L_jj the first entry of CSC column j
 // (kernels.hpp:485-487).
+// scaling_vector (kernels.hpp:299-309) from CSR diagonal positions:
+// d_i = 1 / sqrt(|a_ii|); returns the first row with a zero or missing
+// diagonal, or -1.
+int32_t scaling_vector_csr(const int32_t* diag, const double* vals, int32_t n, double* d,
+                           cudaStream_t s);
 void dscal_vector(const int32_t* colptr, const double* vals, int32_t n,
                   double* d, cudaStream_t s);
 

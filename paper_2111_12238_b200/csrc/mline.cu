@@ -169,16 +169,21 @@ __global__ void __launch_bounds__(kMThreads) k_mline(const MLineArgs A) {
     if (wi >= total)
       break;
     const int item = A.seg_begin + (int)wi;
-    if (S == 1 && A.combo == 4 && item >= A.f_ngroup) {
-      // combo 4 kernel 2: SpMV rows (item - f_ngroup) * 32 + lane as a row
-      // gather over CSR(A) in ascending column order -- the order in which
-      // the sequential CSC scatter (spmv_csc_col, kernels.hpp:162-168)
-      // accumulates y_r, so the sum is the reference's bit for bit.
-      const int r = (item - A.f_ngroup) * 32 + lane;
-      {
+    const bool spmv4 = A.combo == 4 && item >= A.f_ngroup;
+    const bool spmv2 = A.combo == 2 && item < A.f_ngroup;
+    if (S == 1 && (spmv4 || spmv2)) {
+      // SpMV rows blk * 32 + lane as a row gather over CSR(A) in ascending
+      // column order.  Combo 4 kernel 2: the order in which the sequential
+      // CSC scatter (spmv_csc_col, kernels.hpp:162-168) accumulates y_r,
+      // over the solved vector; combo 2 kernel 1: spmv_csr_row
+      // (kernels.hpp:152-158) over the input vector, published for the solve.
+      const int blk = spmv4 ? item - A.f_ngroup : item;
+      const double* xsrc = spmv4 ? A.vmid : A.vin;
+      const int r = blk * 32 + lane;
+      if (spmv4) {
         // one lane watches the block's newest operand (the last row's
         // largest column) with a long back-off before the block gathers
-        const int rl = min((item - A.f_ngroup) * 32 + 31, A.n - 1);
+        const int rl = min(blk * 32 + 31, A.n - 1);
         if (lane == 0) {
           const int pl = __ldg(A.ar_ptr + rl + 1) - 1;
           if (pl >= 0) {
@@ -208,7 +213,7 @@ __global__ void __launch_bounds__(kMThreads) k_mline(const MLineArgs A) {
 #pragma unroll
             for (int a = 0; a < 8; ++a)
               if (a < cnt && (first || is_sent_hi(ww[a]))) {
-                ww[a] = ld_relaxed_u64(A.vmid + jj[a]);
+                ww[a] = ld_relaxed_u64(xsrc + jj[a]);
               }
 #pragma unroll
             for (int a = 0; a < 8; ++a)
@@ -223,7 +228,10 @@ __global__ void __launch_bounds__(kMThreads) k_mline(const MLineArgs A) {
               acc = __dadd_rn(acc, __dmul_rn(__ldg(A.ar_val + p + a),
                                              __longlong_as_double((long long)ww[a])));
         }
-        A.vout[r] = acc;
+        if (spmv4)
+          A.vout[r] = acc;
+        else
+          publish_f64(A.vmid + r, acc);
       }
       continue;
     }

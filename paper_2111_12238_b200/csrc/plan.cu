@@ -131,6 +131,8 @@ template <typename F> sfg_status guarded(sfg_plan* p, F&& f) {
     return set_err(p, SFG_ERR_INVALID_MATRIX, e.what(), SFG_FERR_INVALID_MATRIX, e.index);
   } catch (const InvalidArgument& e) {
     return set_err(p, SFG_ERR_INVALID_ARGUMENT, e.what());
+  } catch (const FactorizationFailure& e) {
+    return set_err(p, SFG_ERR_FACTORIZATION, e.what(), e.kind, e.index);
   } catch (const CudaError& e) {
     return set_err(p, SFG_ERR_CUDA, e.what());
   } catch (const std::bad_alloc&) {
@@ -307,14 +309,21 @@ __global__ void cost_kernel(int kind, int32_t n, const int32_t* __restrict__ ptr
 __global__ void fdep_fill_kernel(int combo, int32_t n, const int32_t* __restrict__ m_ptr,
                                  const int32_t* __restrict__ rv_ptr,
                                  const int32_t* __restrict__ rv_col,
+                                 const int32_t* __restrict__ ar_ptr,
+                                 const int32_t* __restrict__ ar_idx,
                                  const int32_t* __restrict__ rowptr, int32_t* __restrict__ colidx) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     int32_t w = rowptr[i];
     switch (combo) {
     case 1:
+    case 2:
     case 6:
       colidx[w] = (int32_t)i;
+      break;
+    case 3: // dag.hpp:294-302: the DSCAL rows k <= i of A's row i
+      for (int32_t p = ar_ptr[i]; p < ar_ptr[i + 1] && ar_idx[p] <= i; ++p)
+        colidx[w++] = ar_idx[p];
       break;
     case 8:
       colidx[w] = n - 1 - (int32_t)i;
@@ -334,7 +343,9 @@ __global__ void fdep_fill_kernel(int combo, int32_t n, const int32_t* __restrict
 }
 
 __global__ void fdep_count_kernel(int combo, int32_t n, const int32_t* __restrict__ m_ptr,
-                                  const int32_t* __restrict__ rv_ptr, int32_t* __restrict__ cnt) {
+                                  const int32_t* __restrict__ rv_ptr,
+                                  const int32_t* __restrict__ ar_ptr,
+                                  const int32_t* __restrict__ ar_idx, int32_t* __restrict__ cnt) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i <= n;
        i += (int64_t)gridDim.x * blockDim.x) {
     if (i == n) {
@@ -346,6 +357,11 @@ __global__ void fdep_count_kernel(int combo, int32_t n, const int32_t* __restric
       c = m_ptr[i] < m_ptr[i + 1] ? 1 : 0;
     else if (combo == 5 || combo == 7)
       c = rv_ptr[i + 1] - rv_ptr[i] + 1;
+    else if (combo == 3) {
+      c = 0;
+      for (int32_t p = ar_ptr[i]; p < ar_ptr[i + 1] && ar_idx[p] <= i; ++p)
+        ++c;
+    }
     cnt[i] = c;
   }
 }
@@ -414,7 +430,7 @@ void build_plan(sfg_plan* P, const int32_t* colptr, const int32_t* rowidx,
   upload(mval, values, nnzM * S, s);
 
   const int combo = P->combo;
-  if (combo == 1 || combo == 4 || combo == 8 || combo == 5 || combo == 7) {
+  if (combo == 1 || combo == 2 || combo == 4 || combo == 8 || combo == 5 || combo == 7) {
     // lower_triangle (matrix.hpp:98-128)
     DBuf<int32_t> src;
     P->nnzL = lower_triangle(P->m_ptr.p, P->m_idx.p, mval.p, nnzM, S, n, P->lc_ptr,
@@ -429,7 +445,7 @@ void build_plan(sfg_plan* P, const int32_t* colptr, const int32_t* rowidx,
     DBuf<int32_t> csr_ptr((int64_t)n + 1), csr_idx(nnzL > 0 ? nnzL : 1),
         perm(nnzL > 0 ? nnzL : 1), srcc(nnzL > 0 ? nnzL : 1);
     transpose(P->lc_ptr.p, P->lc_idx.p, n, n, nnzL, csr_ptr.p, csr_idx.p, perm.p, s);
-    if (combo == 1 || combo == 4 || combo == 8) {
+    if (combo == 1 || combo == 2 || combo == 4 || combo == 8) {
       compose_kernel<<<grid_for(nnzL), 256, 0, s>>>(src.p, perm.p, nnzL, srcc.p);
       count_launch();
       values_from(mval, nnzM, S, srcc.p, nnzL, P->lr_val, s);
@@ -462,8 +478,9 @@ void build_plan(sfg_plan* P, const int32_t* colptr, const int32_t* rowidx,
       values_from(mval, nnzM, S, srcc.p, nnzL, P->lt_val, s);
       P->map_lt = std::move(srcc);
     }
-    if (combo == 4) {
-      // CSR view of the CSC SpMV operand A = M (row gather, see executor.cu)
+    if (combo == 2 || combo == 4) {
+      // CSR of A: combo 2's SpMV operand (to_csr(M), kernels.hpp:440); for
+      // combo 4 the row view of the CSC SpMV operand (row gather, see mline.cu)
       P->ar_ptr.alloc((int64_t)n + 1);
       P->ar_idx.alloc(nnzM > 0 ? nnzM : 1);
       DBuf<int32_t> aperm(nnzM > 0 ? nnzM : 1);
@@ -480,7 +497,7 @@ void build_plan(sfg_plan* P, const int32_t* colptr, const int32_t* rowidx,
       P->fac.alloc(nnzL > 0 ? nnzL : 1);
       P->work.alloc(nnzL > 0 ? nnzL : 1);
     }
-  } else if (combo == 6) {
+  } else if (combo == 6 || combo == 3) {
     // to_csr(M) (kernels.hpp:475-478) + find_diag_positions
     P->ar_ptr.alloc((int64_t)n + 1);
     P->ar_idx.alloc(nnzM > 0 ? nnzM : 1);
@@ -490,6 +507,13 @@ void build_plan(sfg_plan* P, const int32_t* colptr, const int32_t* rowidx,
     P->map_ar = std::move(aperm);
     P->diag.alloc(n > 0 ? n : 1);
     find_diag_positions(P->ar_ptr.p, P->ar_idx.p, n, P->diag.p, s);
+    if (combo == 3) { // scaling_vector (kernels.hpp:299-309), part of make_state
+      P->dvec.alloc(n > 0 ? n : 1);
+      const int32_t bad = scaling_vector_csr(P->diag.p, P->ar_val.p, n, P->dvec.p, s);
+      if (bad >= 0)
+        throw FactorizationFailure("zero diagonal at index " + std::to_string(bad),
+                                   SFG_FERR_ZERO_DIAG_SCALE, bad);
+    }
     P->nnzF = nnzM;
     P->fac.alloc(nnzM > 0 ? nnzM : 1);
     P->work.alloc(nnzM > 0 ? nnzM : 1);
@@ -497,7 +521,7 @@ void build_plan(sfg_plan* P, const int32_t* colptr, const int32_t* rowidx,
 
   // vectors
   const int64_t nv = (int64_t)n * S;
-  if (combo != 7) {
+  if (combo != 7 && combo != 3) {
     std::vector<double> hv;
     const double* src_h = vin_h;
     if (!vin_h) {
@@ -516,7 +540,7 @@ void build_plan(sfg_plan* P, const int32_t* colptr, const int32_t* rowidx,
     // one extra all-zero row n: the chain-ELL padding reads it
     P->vout.alloc(nv + S);
     SFG_CUDA(cudaMemsetAsync(P->vout.p + nv, 0, sizeof(double) * (size_t)S, s));
-    if (combo == 1 || combo == 4 || combo == 8) {
+    if (combo == 1 || combo == 2 || combo == 4 || combo == 8) {
       P->vmid.alloc(nv + S);
       SFG_CUDA(cudaMemsetAsync(P->vmid.p + nv, 0, sizeof(double) * (size_t)S, s));
     }
@@ -583,11 +607,12 @@ void launch_main(sfg_plan* P, const ExecArgs& a) {
     else
       launch_ic0(P->combo, a, P->stream);
     break;
+  case 3:
   case 6:
     if (P->use_warpfac)
-      launch_ilu0_warp(a, P->upd, P->stream);
+      launch_ilu0_warp(P->combo, a, P->upd, P->stream);
     else
-      launch_ilu0(a, P->stream);
+      launch_ilu0(P->combo, a, P->stream);
     break;
   }
 }
@@ -605,6 +630,7 @@ void do_inspect(sfg_plan* P) {
   const int32_t *ptr = nullptr, *idx = nullptr;
   switch (combo) {
   case 1:
+  case 2:
   case 4:
   case 8:
     ptr = P->lr_ptr.p;
@@ -615,6 +641,7 @@ void do_inspect(sfg_plan* P) {
     ptr = P->rv_ptr.p;
     idx = P->rv_col.p;
     break;
+  case 3:
   case 6:
     ptr = P->ar_ptr.p;
     idx = P->ar_idx.p;
@@ -643,8 +670,8 @@ void do_inspect(sfg_plan* P) {
   // executor choice: the multi-chain warp executor for single-system solve
   // pairs (latency-bound: in-warp dependencies go through shared memory),
   // the chain executor for batched systems; SFG_EXECUTOR overrides
-  const bool want_mline = ex ? std::string(ex) == "mline" : P->nsys == 1;
-  if (want_mline && (combo == 1 || combo == 4 || combo == 8)) {
+  const bool want_mline = (ex ? std::string(ex) == "mline" : P->nsys == 1) || combo == 2;
+  if (want_mline && (combo == 1 || combo == 2 || combo == 4 || combo == 8)) {
     int32_t max_len = 1 << 20;
     if (const char* e = getenv("SFG_CHAIN_MAX"))
       max_len = atoi(e);
@@ -660,7 +687,8 @@ void do_inspect(sfg_plan* P) {
     }
     if (getenv("SFG_TRACE")) {
       P->trace_tiles = 4;
-      const int64_t items = (int64_t)P->ml_f.ngroup + (combo == 8 ? P->ml_b.ngroup : P->ml_f.ngroup);
+      const int64_t items = (int64_t)P->ml_f.ngroup + (n + 31) / 32 +
+                            (combo == 8 ? P->ml_b.ngroup : P->ml_f.ngroup);
       P->trace.alloc(items * 4);
       SFG_CUDA(cudaMemsetAsync(P->trace.p, 0, sizeof(unsigned long long) * items * 4, s));
     }
@@ -671,7 +699,7 @@ void do_inspect(sfg_plan* P) {
     build_ic0_updates(P->lc_ptr.p, P->lc_idx.p, P->rv_ptr.p, P->rv_col.p, P->rv_pos.p, n,
                       P->nnzF, P->upd, s);
     P->use_warpfac = ic0_warp_fits(P->upd);
-  } else if (!legacy && combo == 6) {
+  } else if (!legacy && (combo == 6 || combo == 3)) {
     build_ilu0_updates(P->ar_ptr.p, P->ar_idx.p, P->diag.p, n, P->nnzF, P->upd, s);
     P->use_warpfac = ilu0_warp_fits(P->upd);
   }
@@ -775,6 +803,10 @@ MLineArgs mline_args(sfg_plan* P) {
   a.b_code = L2.code.p;
   a.b_nchain = L2.nchain;
   a.b_ngroup = P->combo == 4 ? (P->n + 31) / 32 : L2.ngroup;
+  if (P->combo == 2) { // SpMV row blocks first, then the solve groups
+    a.f_ngroup = (P->n + 31) / 32;
+    a.b_ngroup = P->ml_f.ngroup;
+  }
   a.vin = P->vin.p;
   a.vmid = P->vmid.p;
   a.vout = P->vout.p;
@@ -878,9 +910,12 @@ void build_g(sfg_plan* P, int which) {
     } else if (c == 7) {
       edgeless(P, *g);
       build_cost(P, CK_ROWNNZ, P->lc_ptr.p, nullptr, nullptr, nullptr, nullptr, *g);
+    } else if (c == 2 || c == 3) { // SpMV_CSR / DSCAL_CSR over A: independent rows
+      edgeless(P, *g);
+      build_cost(P, CK_ROWNNZ, P->ar_ptr.p, nullptr, nullptr, nullptr, nullptr, *g);
     }
   } else { // build_g2 (dag.hpp:339-370)
-    if (c == 1) {
+    if (c == 1 || c == 2) {
       dag_from_structure(P, P->lr_ptr.p, P->lr_idx.p, P->nnzL, EM_ROWS_LOWER, *g);
       build_cost(P, CK_ROWNNZ, P->lr_ptr.p, nullptr, nullptr, nullptr, nullptr, *g);
     } else if (c == 4) {
@@ -892,6 +927,9 @@ void build_g(sfg_plan* P, int which) {
     } else if (c == 6) {
       dag_from_structure(P, P->ar_ptr.p, P->ar_idx.p, P->nnzM, EM_ROWS_LOWER, *g);
       build_cost(P, CK_UNIT, P->ar_ptr.p, P->ar_idx.p, nullptr, nullptr, nullptr, *g);
+    } else if (c == 3) { // SpILU0_CSR over A
+      dag_from_structure(P, P->ar_ptr.p, P->ar_idx.p, P->nnzM, EM_ROWS_LOWER, *g);
+      build_cost(P, CK_ILU0, P->ar_ptr.p, P->ar_idx.p, nullptr, P->diag.p, nullptr, *g);
     } else if (c == 7) {
       dag_from_structure(P, P->lc_ptr.p, P->lc_idx.p, P->nnzL, EM_COLS_BELOW, *g);
       build_cost(P, CK_IC0, P->lc_ptr.p, nullptr, P->rv_ptr.p, P->rv_col.p, P->rv_pos.p, *g);
@@ -913,7 +951,8 @@ void build_fdep(sfg_plan* P) {
   f->ptr.alloc((int64_t)n + 1);
   DBuf<int32_t> cnt((int64_t)n + 1);
   fdep_count_kernel<<<grid_for((int64_t)n + 1), 256, 0, s>>>(P->combo, n, P->m_ptr.p,
-                                                              P->rv_ptr.p, cnt.p);
+                                                              P->rv_ptr.p, P->ar_ptr.p,
+                                                              P->ar_idx.p, cnt.p);
   count_launch();
   size_t bytes = 0;
   SFG_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, bytes, cnt.p, f->ptr.p, n + 1, s));
@@ -925,7 +964,8 @@ void build_fdep(sfg_plan* P) {
   f->nedges = nnz;
   f->idx.alloc(nnz > 0 ? nnz : 1);
   fdep_fill_kernel<<<grid_for(n), 256, 0, s>>>(P->combo, n, P->m_ptr.p, P->rv_ptr.p,
-                                               P->rv_col.p, f->ptr.p, f->idx.p);
+                                               P->rv_col.p, P->ar_ptr.p, P->ar_idx.p, f->ptr.p,
+                                               f->idx.p);
   count_launch();
   SFG_CUDA(cudaStreamSynchronize(s));
   P->fdep = std::move(f);
@@ -1007,6 +1047,7 @@ int ferr_kind_of(int combo, int kernel) {
   switch (combo) {
   case 5:
     return kernel == 1 ? SFG_FERR_NONPOS_PIVOT : SFG_FERR_ZERO_DIAG_SOLVE;
+  case 3:
   case 6:
     return SFG_FERR_ZERO_PIVOT;
   case 7:
@@ -1053,6 +1094,7 @@ void exec_fused_impl(sfg_plan* P, cudaEvent_t kb, cudaEvent_t ke) {
   int nr = 0;
   switch (P->combo) {
   case 1:
+  case 2:
   case 8:
     r[nr++] = {P->vmid.p, nv};
     r[nr++] = {P->vout.p, nv};
@@ -1065,6 +1107,7 @@ void exec_fused_impl(sfg_plan* P, cudaEvent_t kb, cudaEvent_t ke) {
     r[nr++] = {P->fac.p, P->nnzF};
     r[nr++] = {P->vout.p, nv};
     break;
+  case 3:
   case 7:
     r[nr++] = {P->fac.p, P->nnzF};
     break;
@@ -1106,7 +1149,7 @@ void exec_unfused_impl(sfg_plan* P, cudaEvent_t kb, cudaEvent_t ke) {
   ExecArgs a = exec_args(P);
   FillRegion r1[2];
   int n1 = 0;
-  if (c == 1 || c == 4 || c == 8)
+  if (c == 1 || c == 2 || c == 4 || c == 8)
     r1[n1++] = {P->vmid.p, nv};
   else if (c == 5 || c == 6)
     r1[n1++] = {P->fac.p, P->nnzF};
@@ -1163,13 +1206,15 @@ void exec_unfused_impl(sfg_plan* P, cudaEvent_t kb, cudaEvent_t ke) {
   a.t_end = n;
   if (c == 7)
     launch_dscal(a, P->stream);
+  else if (c == 3)
+    launch_dscal_csr(a, P->stream);
   else
     launch_main(P, a);
   FillRegion r2[2];
   int n2 = 0;
   if (c == 1 || c == 8 || c == 5 || c == 6)
     r2[n2++] = {P->vout.p, nv};
-  else if (c == 7)
+  else if (c == 7 || c == 3)
     r2[n2++] = {P->fac.p, P->nnzF};
   launch_prep(r2, n2, P->counter.p, nullptr, P->stream);
   a.phase = 2;
@@ -1244,7 +1289,7 @@ sfg_status sfg_plan_create(int32_t combo, int32_t n, const int32_t* colptr,
   if (!out)
     return SFG_ERR_INVALID_ARGUMENT;
   *out = nullptr;
-  if (!(combo == 1 || combo == 4 || combo == 5 || combo == 6 || combo == 7 || combo == 8))
+  if (combo < 1 || combo > 8)
     return SFG_ERR_INVALID_ARGUMENT;
   if (n < 0 || !colptr || (colptr[n] > 0 && (!rowidx || !values)))
     return SFG_ERR_INVALID_ARGUMENT;
@@ -1353,13 +1398,13 @@ sfg_status sfg_plan_info(const sfg_plan* P, int32_t* combo, int32_t* n, int32_t*
     *nnz_factor = P->nnzF;
   if (out_len) {
     const int c = P->combo;
-    *out_len = (c == 1 || c == 4 || c == 8) ? 2 * (int64_t)P->n : P->nnzF + P->n;
+    *out_len = (c == 1 || c == 2 || c == 4 || c == 8) ? 2 * (int64_t)P->n : P->nnzF + P->n;
   }
   return SFG_OK;
 }
 
 sfg_status sfg_set_vin(sfg_plan* P, const double* vin_host) {
-  if (!P || !vin_host || P->combo == 7)
+  if (!P || !vin_host || P->combo == 7 || P->combo == 3)
     return SFG_ERR_INVALID_ARGUMENT;
   return guarded(P, [&] {
     DeviceScope ds(P->device);
@@ -1412,7 +1457,7 @@ sfg_status sfg_set_values(sfg_plan* P, const double* values_host) {
     SFG_CUDA(cudaMemcpyAsync(P->mstage.p, values_host, sizeof(double) * (size_t)tot,
                              cudaMemcpyHostToDevice, s));
     const int c = P->combo;
-    if (c != 6) {
+    if (c != 6 && c != 3) {
       DBuf<unsigned long long> bad(1);
       SFG_CUDA(cudaMemsetAsync(bad.p, 0xFF, sizeof(unsigned long long), s));
       diag_check_kernel<<<grid_for((int64_t)n * S), 256, 0, s>>>(P->mstage.p, nnzM, S,
@@ -1429,14 +1474,20 @@ sfg_status sfg_set_values(sfg_plan* P, const double* values_host) {
       }
     }
     const int64_t nnzL = P->nnzL;
-    if (c == 1 || c == 4 || c == 8)
+    if (c == 1 || c == 2 || c == 4 || c == 8)
       gather_values(P->mstage.p, nnzM, P->map_lr.p, nnzL, S, P->lr_val.p, s);
     if (c == 8)
       gather_values(P->mstage.p, nnzM, P->map_lt.p, nnzL, S, P->lt_val.p, s);
     if (c == 5 || c == 7)
       gather_values(P->mstage.p, nnzM, P->map_lc.p, nnzL, S, P->lc_val.p, s);
-    if (c == 4 || c == 6)
+    if (c == 2 || c == 3 || c == 4 || c == 6)
       gather_values(P->mstage.p, nnzM, P->map_ar.p, nnzM, 1, P->ar_val.p, s);
+    if (c == 3) {
+      const int32_t bad = scaling_vector_csr(P->diag.p, P->ar_val.p, n, P->dvec.p, s);
+      if (bad >= 0)
+        throw FactorizationFailure("zero diagonal at index " + std::to_string(bad),
+                                   SFG_FERR_ZERO_DIAG_SCALE, bad);
+    }
     if (c == 7)
       dscal_vector(P->lc_ptr.p, P->lc_val.p, n, P->dvec.p, s);
     if (P->use_ell) { // the chain-ELL records hold copies of the values
@@ -1547,8 +1598,12 @@ sfg_status sfg_compute_reuse(sfg_plan* P, double* reuse) {
   case 8:
     *reuse = (2 * dn + 2 * L) / std::max(2 * dn + L, L + 2 * dn);
     break;
+  case 2:
   case 4:
     *reuse = 2 * dn / std::max(2 * dn + L, A + 2 * dn);
+    break;
+  case 3:
+    *reuse = 2 * A / std::max(A, A + 2 * dn);
     break;
   case 5:
   case 7:
@@ -1601,8 +1656,19 @@ sfg_status sfg_get_schedule(sfg_plan* P, int64_t* nentries, uint8_t* tags, int32
           wp.push_back((int64_t)tg.size());
         }
       };
-      emit(P->ml_f, 1);
-      if (P->combo == 4) { // SpMV rows after every forward row
+      if (P->combo == 2) { // SpMV rows first, then the solve groups
+        for (int32_t r = 0; r < P->n; ++r) {
+          tg.push_back(1);
+          it.push_back(r);
+          if ((r & 31) == 31 || r == P->n - 1)
+            wp.push_back((int64_t)tg.size());
+        }
+        emit(P->ml_f, 2);
+      } else {
+        emit(P->ml_f, 1);
+      }
+      if (P->combo == 2) {
+      } else if (P->combo == 4) { // SpMV rows after every forward row
         for (int32_t r = 0; r < P->n; ++r) {
           tg.push_back(2);
           it.push_back(r);
@@ -1785,7 +1851,7 @@ sfg_status sfg_collect_outputs(sfg_plan* P, double* out, int64_t cap) {
     const int c = P->combo;
     const int32_t n = P->n, S = P->nsys;
     cudaStream_t s = P->stream;
-    if (c == 1 || c == 4 || c == 8) {
+    if (c == 1 || c == 2 || c == 4 || c == 8) {
       const int64_t need = 2 * (int64_t)n * S;
       if (cap < need)
         throw InvalidArgument("output buffer too small");
@@ -1810,7 +1876,7 @@ sfg_status sfg_collect_outputs(sfg_plan* P, double* out, int64_t cap) {
       if (P->nnzF)
         SFG_CUDA(cudaMemcpyAsync(out, P->fac.p, sizeof(double) * (size_t)P->nnzF,
                                  cudaMemcpyDeviceToHost, s));
-      const double* tail = c == 7 ? P->dvec.p : P->vout.p;
+      const double* tail = (c == 7 || c == 3) ? P->dvec.p : P->vout.p;
       if (n)
         SFG_CUDA(cudaMemcpyAsync(out + P->nnzF, tail, sizeof(double) * (size_t)n,
                                  cudaMemcpyDeviceToHost, s));
@@ -1825,7 +1891,7 @@ sfg_status sfg_device_output(sfg_plan* P, int32_t which, void** dptr, int64_t* c
     return SFG_ERR_INVALID_ARGUMENT;
   const int c = P->combo;
   const int64_t nv = (int64_t)P->n * P->nsys;
-  if (c == 1 || c == 4 || c == 8) {
+  if (c == 1 || c == 2 || c == 4 || c == 8) {
     *dptr = which == 0 ? (void*)P->vmid.p : (void*)P->vout.p;
     if (count)
       *count = nv;
@@ -1835,7 +1901,7 @@ sfg_status sfg_device_output(sfg_plan* P, int32_t which, void** dptr, int64_t* c
       if (count)
         *count = P->nnzF;
     } else {
-      *dptr = c == 7 ? (void*)P->dvec.p : (void*)P->vout.p;
+      *dptr = (c == 7 || c == 3) ? (void*)P->dvec.p : (void*)P->vout.p;
       if (count)
         *count = P->n;
     }

@@ -213,6 +213,18 @@ __global__ void dscal_vector_kernel(const int32_t* __restrict__ colptr,
     d[j] = __ddiv_rn(1.0, __dsqrt_rn(fabs(vals[colptr[j]])));
 }
 
+__global__ void scaling_csr_kernel(const int32_t* __restrict__ diag,
+                                   const double* __restrict__ vals, int32_t n,
+                                   double* __restrict__ d, int* bad) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const double a = diag[i] >= 0 ? vals[diag[i]] : 0.0;
+    if (a == 0.0)
+      atomicMin(bad, (int)i);
+    d[i] = __ddiv_rn(1.0, __dsqrt_rn(fabs(a)));
+  }
+}
+
 __global__ void interleave_kernel(const double* __restrict__ in, int32_t n,
                                   int32_t nsys, double* __restrict__ out,
                                   int to_inter) {
@@ -313,6 +325,24 @@ void find_diag_positions(const int32_t* rowptr, const int32_t* colidx,
   find_diag_kernel<<<grid_for(n), 256, 0, s>>>(rowptr, colidx, n, diag);
   count_launch();
   SFG_CUDA(cudaGetLastError());
+}
+
+int32_t scaling_vector_csr(const int32_t* diag, const double* vals, int32_t n, double* d,
+                           cudaStream_t s) {
+  if (n == 0)
+    return -1;
+  int* bad = nullptr;
+  SFG_CUDA(cudaMallocAsync(&bad, sizeof(int), s));
+  const int init = 0x7fffffff;
+  SFG_CUDA(cudaMemcpyAsync(bad, &init, sizeof(int), cudaMemcpyHostToDevice, s));
+  scaling_csr_kernel<<<grid_for(n), 256, 0, s>>>(diag, vals, n, d, bad);
+  count_launch();
+  SFG_CUDA(cudaGetLastError());
+  int h = init;
+  SFG_CUDA(cudaMemcpyAsync(&h, bad, sizeof(int), cudaMemcpyDeviceToHost, s));
+  SFG_CUDA(cudaFreeAsync(bad, s));
+  SFG_CUDA(cudaStreamSynchronize(s));
+  return h == init ? -1 : h;
 }
 
 void dscal_vector(const int32_t* colptr, const double* vals, int32_t n,

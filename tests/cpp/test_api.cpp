@@ -80,7 +80,7 @@ int main(int argc, char** argv) {
     std::printf("%s (no device: %d)\n", failures ? "FAILED" : "OK", (int)!device);
     return failures ? 1 : 0;
   }
-  for (int combo : {1, 4, 5, 6, 7, 8}) {
+  for (int combo : {1, 2, 3, 4, 5, 6, 7, 8}) {
     auto st = sf::make_state(combo, M, 7);
     if (combo != 8) {
       orc_dag w1{}, w2{}, wj{};

@@ -46,8 +46,9 @@ def test_invalid_arguments_rejected_before_device():
     cp = np.array([0, 1], np.int32)
     ri = np.array([0], np.int32)
     va = np.array([1.0])
-    # combo 2 / 3 are not served by this executor; nsys > 1 only for 1 and 8
-    assert L.sfg_plan_create(2, 1, abi.ptr(cp, abi.i32p), abi.ptr(ri, abi.i32p),
-                             abi.ptr(va, abi.f64p), 1, None, 7, C.byref(h)) == abi.SFG_ERR_INVALID_ARGUMENT
+    # combo ids outside 1..8 are rejected; nsys > 1 only for 1 and 8
+    for bad in (0, 9):
+        assert L.sfg_plan_create(bad, 1, abi.ptr(cp, abi.i32p), abi.ptr(ri, abi.i32p),
+                                 abi.ptr(va, abi.f64p), 1, None, 7, C.byref(h)) == abi.SFG_ERR_INVALID_ARGUMENT
     assert L.sfg_plan_create(5, 1, abi.ptr(cp, abi.i32p), abi.ptr(ri, abi.i32p),
                              abi.ptr(va, abi.f64p), 2, None, 7, C.byref(h)) == abi.SFG_ERR_INVALID_ARGUMENT

@@ -2,7 +2,7 @@
 
 tests/cpp/test_api.cpp is compiled against the header, libsfgpu.so and the C
 oracle, then run: without a GPU it must refuse to compute (NoDeviceError, no
-CPU fallback); on a B200 it drives combos 1, 4-8 through make_state ->
+CPU fallback); on a B200 it drives combos 1-8 through make_state ->
 build_g1/g2 -> inter_dag -> joint_dag -> level_info -> make_fused_schedule ->
 execute_fused / execute_unfused -> collect_outputs and checks each result bit
 for bit against the oracle, plus the FactorizationError / InvalidMatrixError
@@ -40,6 +40,6 @@ def test_cpp_api_end_to_end(tmp_path):
     r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout + r.stderr
     assert r.stdout.strip().splitlines()[-1] == "OK"
-    for combo in (1, 4, 5, 6, 7, 8):
+    for combo in (1, 2, 3, 4, 5, 6, 7, 8):
         assert f"combo {combo}:" in r.stdout
     assert "breakdown:" in r.stdout

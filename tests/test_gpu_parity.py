@@ -18,7 +18,7 @@ from oracle.oracle import Csc
 
 pytestmark = pytest.mark.gpu
 
-GPU_COMBOS = (1, 4, 5, 6, 7, 8)
+GPU_COMBOS = (1, 2, 3, 4, 5, 6, 7, 8)
 TOL = 1e-10  # north_star: fp64 values within max-relative-error 1e-10
 
 
@@ -54,7 +54,7 @@ def test_golden_outputs_fused_and_unfused(golden, name, combo):
 
 
 @pytest.mark.parametrize("name", GOLDEN_MATS)
-@pytest.mark.parametrize("combo", (1, 4, 5, 6, 7))
+@pytest.mark.parametrize("combo", (1, 2, 3, 4, 5, 6, 7))
 def test_golden_dags_levels(golden, name, combo):
     M = as_sf(golden_matrix(golden, name))
     key = f"{name}/c{combo}"
@@ -96,7 +96,7 @@ def _check_linear_extension(st, joint):
 
 
 @pytest.mark.parametrize("name", GOLDEN_MATS)
-@pytest.mark.parametrize("combo", (1, 4, 5, 6, 7))
+@pytest.mark.parametrize("combo", (1, 2, 3, 4, 5, 6, 7))
 def test_schedule_is_linear_extension(golden, name, combo):
     M = as_sf(golden_matrix(golden, name))
     st = sf.make_state(combo, M).inspect()
@@ -143,6 +143,36 @@ def test_zero_diagonal_solve_error(orc, combo):
     vals[p] = 0.0
     with pytest.raises(sf.InvalidMatrixError, match="zero diagonal entry at column 9"):
         sf.make_state(combo, sf.CscMatrix(M.n, M.colptr, M.rowidx, vals))
+
+
+def test_combo3_zero_diagonal_is_factorization_error(orc):
+    # scaling_vector throws from make_state (kernels.hpp:299-309)
+    M = sf.config_matrix(3, size=6)
+    vals = M.values.copy()
+    j = 11
+    p = M.colptr[j] + list(M.rowidx[M.colptr[j]:M.colptr[j + 1]]).index(j)
+    vals[p] = 0.0
+    Mo = Csc(M.n, M.colptr, M.rowidx, vals)
+    from oracle.oracle import FactorizationError as OFE
+    with pytest.raises(OFE) as want:
+        orc.run_sequential(3, Mo, 7)
+    with pytest.raises(sf.FactorizationError) as got:
+        sf.make_state(3, as_sf(Mo))
+    assert got.value.index == want.value.index == 11
+    assert "zero diagonal" in str(got.value)
+
+
+@pytest.mark.parametrize("combo", (2, 3))
+def test_combos_2_3_full_size_vs_oracle(orc, combo):
+    # the reference's remaining Table-2 pairs on the BASELINE matrices
+    M = sf.config_matrix(1 if combo == 2 else 3)
+    Mo = Csc(M.n, M.colptr, M.rowidx, M.values)
+    want = orc.run_sequential(combo, Mo, 7)
+    st = sf.make_state(combo, M, seed=7)
+    st.execute_fused()
+    assert np.array_equal(st.collect_outputs(), want)
+    st.execute_unfused()
+    assert np.array_equal(st.collect_outputs(), want)
 
 
 def test_ilu0_zero_pivot_index(orc):
