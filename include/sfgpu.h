@@ -128,6 +128,18 @@ sfg_status sfg_get_schedule(sfg_plan* plan, int64_t* nentries,
                             uint8_t* tags, int32_t* iters, int32_t* nwaves,
                             int64_t* wave_ptr);
 
+/* The same schedule as the reference's FusedPartitioning (msp.hpp:44-63), so
+ * validate_fused_partitioning (msp.hpp:1108-1237) can check it: nspart
+ * s-partitions executed in order, s-partition k holding w-partitions
+ * [s_ptr[k], s_ptr[k+1]) that are mutually independent, w-partition w holding
+ * entries [w_ptr[w], w_ptr[w+1]) in execution order (tag 1/2 = kernel,
+ * iter = iteration; combo 8's kernel-2 iterations use i' = n-1-i).  The
+ * s-partitions are the executor's dependency levels (chain, group or task
+ * levels); the GPU itself runs them without barriers.  Two-phase. */
+sfg_status sfg_get_partitioning(sfg_plan* plan, int32_t* nspart, int64_t* nwpart,
+                                int64_t* nentries, int64_t* s_ptr, int64_t* w_ptr,
+                                uint8_t* tags, int32_t* iters);
+
 /* Executor (replaces execute_fused / execute_unfused, executor.hpp:325-461)
  * Asynchronous on the plan stream. */
 sfg_status sfg_execute_fused(sfg_plan* plan);

@@ -355,6 +355,53 @@ inline FusedSchedule make_fused_schedule(KernelState& st, Index /*r*/ = 0,
   return fs;
 }
 
+// FusedEntry / FusedPartitioning (msp.hpp:19-63): the same schedule as nested
+// s-partitions (run in order) of independent w-partitions (ordered entries),
+// checkable with the reference's validate_fused_partitioning.
+struct FusedEntry {
+  std::uint8_t tag = 1;
+  Index iter = 0;
+  bool dup = false;
+};
+struct FusedPartitioning {
+  bool fusion = true;
+  bool interleaved = false;
+  double reuse_ratio = 0.0;
+  Index n1 = 0, n2 = 0;
+  std::vector<std::vector<std::vector<FusedEntry>>> spartitions;
+  Index b() const { return static_cast<Index>(spartitions.size()); }
+};
+
+inline FusedPartitioning fused_partitioning(KernelState& st) {
+  st.inspect();
+  std::int32_t ns = 0;
+  std::int64_t nw = 0, ne = 0;
+  detail::check(st.handle(),
+                sfg_get_partitioning(st.handle(), &ns, &nw, &ne, nullptr, nullptr, nullptr,
+                                     nullptr),
+                "partitioning");
+  std::vector<std::int64_t> sp((size_t)ns + 1), wp((size_t)nw + 1);
+  std::vector<std::uint8_t> tg((size_t)ne);
+  std::vector<Index> it((size_t)ne);
+  detail::check(st.handle(),
+                sfg_get_partitioning(st.handle(), nullptr, nullptr, nullptr, sp.data(),
+                                     wp.data(), tg.data(), it.data()),
+                "partitioning");
+  FusedPartitioning V;
+  V.reuse_ratio = compute_reuse(st);
+  V.interleaved = V.reuse_ratio >= 1.0;
+  V.n1 = V.n2 = st.n;
+  V.spartitions.resize((size_t)ns);
+  for (std::int32_t k = 0; k < ns; ++k)
+    for (std::int64_t w = sp[(size_t)k]; w < sp[(size_t)k + 1]; ++w) {
+      std::vector<FusedEntry> es;
+      for (std::int64_t e = wp[(size_t)w]; e < wp[(size_t)w + 1]; ++e)
+        es.push_back(FusedEntry{tg[(size_t)e], it[(size_t)e], false});
+      V.spartitions[(size_t)k].push_back(std::move(es));
+    }
+  return V;
+}
+
 namespace detail {
 inline ExecStats finish(KernelState& st, std::int64_t launches0) {
   detail::check(st.handle(), sfg_synchronize(st.handle()), "execute");

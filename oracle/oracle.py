@@ -291,6 +291,9 @@ class Reference:
         L.ref_compute_reuse.restype = C.c_double
         L.ref_wavefront.argtypes = [vp, C.POINTER(C.c_uint8), _i32p, _i32p, _i32p]
         L.ref_wavefront.restype = C.c_int64
+        L.ref_validate_partitioning.argtypes = [vp, C.c_int32, _i64p, _i64p,
+                                                C.POINTER(C.c_uint8), _i32p, C.c_char_p, C.c_int]
+        L.ref_validate_partitioning.restype = C.c_int64
         self.lib = L
 
     # ---- fixtures.hpp
@@ -413,6 +416,19 @@ class RefState:
         if rc:
             raise ValueError(msg.value.decode())
         return out[:L.ref_output_len(self.h)]
+
+    def validate_partitioning(self, s_ptr, w_ptr, tags, iters) -> tuple:
+        """validate_fused_partitioning (msp.hpp:1108-1237) of an external
+        partitioning in flat form; returns (violations, first message)."""
+        sp = np.ascontiguousarray(s_ptr, np.int64)
+        wp = np.ascontiguousarray(w_ptr, np.int64)
+        tg = np.ascontiguousarray(tags, np.uint8)
+        it = np.ascontiguousarray(iters, np.int32)
+        msg = C.create_string_buffer(512)
+        nbad = self.ref.lib.ref_validate_partitioning(
+            self.h, len(sp) - 1, _p(sp, _i64p), _p(wp, _i64p),
+            tg.ctypes.data_as(C.POINTER(C.c_uint8)), _p(it, _i32p), msg, 512)
+        return int(nbad), msg.value.decode()
 
     def bench(self, executor: int, nthreads: int, warmups: int = 2, repeats: int = 5):
         """Returns (per-repeat seconds, inspector seconds, s-partitions)."""

@@ -355,4 +355,33 @@ int64_t ref_wavefront(void* s, uint8_t* tags, int32_t* iters,
   return static_cast<int64_t>(ws.entries.size());
 }
 
+// validate_fused_partitioning (msp.hpp:1108-1237) of a partitioning built
+// elsewhere (the GPU inspector): s-partition k = w-partitions
+// [s_ptr[k], s_ptr[k+1]), w-partition w = entries [w_ptr[w], w_ptr[w+1]).
+// Returns the number of violations; the first one goes to msg.
+int64_t ref_validate_partitioning(void* s, int32_t nspart, const int64_t* s_ptr,
+                                  const int64_t* w_ptr, const uint8_t* tags,
+                                  const int32_t* iters, char* msg, int ml) {
+  auto* st = static_cast<KernelState*>(s);
+  const Setup su = inspect(*st);
+  FusedPartitioning V;
+  V.fusion = true;
+  V.reuse_ratio = su.reuse;
+  V.interleaved = su.reuse >= 1.0;
+  V.n1 = su.g1.nvert;
+  V.n2 = su.g2.nvert;
+  V.spartitions.resize((std::size_t)nspart);
+  for (int32_t k = 0; k < nspart; ++k)
+    for (int64_t w = s_ptr[k]; w < s_ptr[k + 1]; ++w) {
+      std::vector<FusedEntry> es;
+      for (int64_t e = w_ptr[w]; e < w_ptr[w + 1]; ++e)
+        es.push_back(FusedEntry{tags[e], iters[e], false});
+      V.spartitions[(std::size_t)k].push_back(std::move(es));
+    }
+  const std::vector<std::string> bad = validate_fused_partitioning(V, su.g1, su.g2, su.f);
+  if (!bad.empty())
+    put_msg(msg, ml, bad.front() + " (" + std::to_string(bad.size()) + " violations)");
+  return (int64_t)bad.size();
+}
+
 } // extern "C"

@@ -116,6 +116,32 @@ class FusedSchedule:
         return len(self.wave_ptr) - 1
 
 
+@dataclass
+class FusedPartitioning:
+    """FusedPartitioning (msp.hpp:44-63) in flat form: s-partition k holds
+    w-partitions [s_ptr[k], s_ptr[k+1]); w-partition w holds the ordered
+    (tag, iter) entries [w_ptr[w], w_ptr[w+1])."""
+
+    s_ptr: np.ndarray
+    w_ptr: np.ndarray
+    tags: np.ndarray
+    iters: np.ndarray
+
+    def b(self) -> int:
+        return len(self.s_ptr) - 1
+
+    def spartitions(self):
+        """Nested [s][w] lists of (tag, iter), the reference's layout."""
+        out = []
+        for k in range(self.b()):
+            ws = []
+            for w in range(self.s_ptr[k], self.s_ptr[k + 1]):
+                e0, e1 = self.w_ptr[w], self.w_ptr[w + 1]
+                ws.append(list(zip(self.tags[e0:e1].tolist(), self.iters[e0:e1].tolist())))
+            out.append(ws)
+        return out
+
+
 def _raise(L, h, st: int, what: str):
     if st == abi.SFG_OK:
         return
@@ -256,6 +282,24 @@ class KernelState:
         self._chk(self.L.sfg_get_schedule(self.h, None, ptr(tags, u8p), ptr(iters, i32p), None,
                                           ptr(wp, i64p)), "schedule")
         return FusedSchedule(tags[:ne.value], iters[:ne.value], wp)
+
+    def partitioning(self) -> "FusedPartitioning":
+        """The schedule as the reference's FusedPartitioning (msp.hpp:44-63)."""
+        if not self.inspected:
+            self.inspect()
+        ns = C.c_int32()
+        nw = C.c_int64()
+        ne = C.c_int64()
+        self._chk(self.L.sfg_get_partitioning(self.h, C.byref(ns), C.byref(nw), C.byref(ne),
+                                              None, None, None, None), "partitioning")
+        sp = np.empty(ns.value + 1, np.int64)
+        wp = np.empty(nw.value + 1, np.int64)
+        tags = np.empty(max(ne.value, 1), np.uint8)
+        iters = np.empty(max(ne.value, 1), np.int32)
+        self._chk(self.L.sfg_get_partitioning(self.h, None, None, None, ptr(sp, i64p),
+                                              ptr(wp, i64p), ptr(tags, u8p), ptr(iters, i32p)),
+                  "partitioning")
+        return FusedPartitioning(sp, wp, tags[:ne.value], iters[:ne.value])
 
     # ---- executor
     def execute_fused(self, sync: bool = True):

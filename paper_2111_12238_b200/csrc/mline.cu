@@ -536,6 +536,8 @@ void build_mline(const int32_t* ptr, const int32_t* idx, int32_t n, int dir, int
   out.nlevels = levels_syncfree(gd.ptr.p, gd.idx.p, ng, +1, level.p, s);
   out.gorder.alloc(ng);
   order_by_level(level.p, ng, out.nlevels, out.gorder.p, nullptr, s);
+  SFG_CUDA(cudaStreamSynchronize(s));
+  out.glevel = std::move(level);
   // longest group (diagnostics)
   std::vector<int32_t> hs((size_t)ng);
   SFG_CUDA(cudaMemcpyAsync(hs.data(), out.gsteps.p, sizeof(int32_t) * (size_t)ng,

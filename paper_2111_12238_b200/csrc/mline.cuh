@@ -37,6 +37,7 @@ struct MLineLayout {
   DBuf<int32_t> cskew;  // chain -> step of its offset 0 within the group
   DBuf<int32_t> gsteps; // group -> steps to run
   DBuf<int32_t> gorder; // groups in claim order (group-DAG level, id)
+  DBuf<int32_t> glevel; // group -> group-DAG level (1-based)
   DBuf<int32_t> code;   // per CSR entry: >= 0 external row index, < 0 ring
                         // code -1 - (delta * 32 + b') (delta < kRing)
 };

@@ -1797,6 +1797,167 @@ sfg_status sfg_get_schedule(sfg_plan* P, int64_t* nentries, uint8_t* tags, int32
   });
 }
 
+namespace {
+
+// The executor's schedule as the reference's FusedPartitioning (msp.hpp:44-63):
+// s-partitions run one after another, their w-partitions are independent and
+// each w-partition is an ordered list of (kernel, iteration) entries.  Every
+// executor here orders its work by a dependency level (chain-DAG or group-DAG
+// level for the solve executors, task level for the others), so the levels
+// are the s-partitions and the sequential work units -- a chain, a group in
+// step order, a fused task, a block of SpMV rows -- the w-partitions.
+struct Partition {
+  std::vector<int64_t> s_ptr{0}, w_ptr{0};
+  std::vector<uint8_t> tags;
+  std::vector<int32_t> iters;
+  void entry(uint8_t t, int32_t i) {
+    tags.push_back(t);
+    iters.push_back(i);
+  }
+  void end_w() { w_ptr.push_back((int64_t)tags.size()); }
+  void end_s() {
+    if ((int64_t)w_ptr.size() - 1 > s_ptr.back())
+      s_ptr.push_back((int64_t)w_ptr.size() - 1);
+  }
+};
+
+std::vector<int32_t> fetch_i32(const DBuf<int32_t>& d, int64_t cnt) {
+  std::vector<int32_t> h((size_t)std::max<int64_t>(cnt, 0));
+  if (cnt > 0)
+    SFG_CUDA(cudaMemcpy(h.data(), d.p, sizeof(int32_t) * (size_t)cnt, cudaMemcpyDeviceToHost));
+  return h;
+}
+
+void spmv_blocks(Partition& V, int32_t n, uint8_t tag) {
+  for (int32_t r0 = 0; r0 < n; r0 += 32) {
+    for (int32_t r = r0; r < std::min(n, r0 + 32); ++r)
+      V.entry(tag, r);
+    V.end_w();
+  }
+  V.end_s();
+}
+
+void mline_groups(Partition& V, const MLineLayout& L, uint8_t tag) {
+  const auto lev = fetch_i32(L.glevel, L.ngroup);
+  const auto go = fetch_i32(L.gorder, L.ngroup);
+  const auto gs = fetch_i32(L.gsteps, L.ngroup);
+  const auto cs = fetch_i32(L.cstart, (int64_t)L.nchain + 1);
+  const auto sk = fetch_i32(L.cskew, L.nchain);
+  int32_t cur = -1;
+  for (int32_t q = 0; q < L.ngroup; ++q) {
+    const int32_t g = go[(size_t)q];
+    if (lev[(size_t)g] != cur) {
+      V.end_s();
+      cur = lev[(size_t)g];
+    }
+    const int32_t c0 = g * L.B, c1 = std::min(L.nchain, c0 + L.B);
+    for (int32_t st = 0; st < gs[(size_t)g]; ++st)
+      for (int32_t c = c0; c < c1; ++c) {
+        const int32_t o = st - sk[(size_t)c];
+        if (o >= 0 && o < cs[(size_t)c + 1] - cs[(size_t)c])
+          V.entry(tag, cs[(size_t)c] + o);
+      }
+    V.end_w();
+  }
+  V.end_s();
+}
+
+void chain_levels(Partition& V, const ChainLayout& L, uint8_t tag, bool with_second) {
+  const auto lev = fetch_i32(L.clevel, L.nchain);
+  const auto co = fetch_i32(L.corder, L.nchain);
+  const auto cs = fetch_i32(L.cstart, (int64_t)L.nchain + 1);
+  int32_t cur = -1;
+  for (int32_t q = 0; q < L.nchain; ++q) {
+    const int32_t c = co[(size_t)q];
+    if (lev[(size_t)c] != cur) {
+      V.end_s();
+      cur = lev[(size_t)c];
+    }
+    for (int32_t p = cs[(size_t)c]; p < cs[(size_t)c + 1]; ++p) {
+      V.entry(tag, p);
+      if (with_second)
+        V.entry(2, p);
+    }
+    V.end_w();
+  }
+  V.end_s();
+}
+
+void build_partition(sfg_plan* P, Partition& V) {
+  const int c = P->combo;
+  const int32_t n = P->n;
+  if (P->use_mline) {
+    if (c == 2) {
+      spmv_blocks(V, n, 1);
+      mline_groups(V, P->ml_f, 2);
+    } else {
+      mline_groups(V, P->ml_f, 1);
+      if (c == 4)
+        spmv_blocks(V, n, 2);
+      else
+        mline_groups(V, c == 8 ? P->ml_b : P->ml_f, 2);
+    }
+    return;
+  }
+  if (P->use_chain || P->use_ell) {
+    chain_levels(V, P->ch_f, 1, c == 1);
+    if (c == 8)
+      chain_levels(V, P->ch_b, 2, false);
+    else if (c == 4)
+      spmv_blocks(V, n, 2);
+    return;
+  }
+  // ticket executors: one s-partition per wavefront, one task per w-partition
+  const bool fused_task = !(c == 4 || c == 8);
+  const auto ord = fetch_i32(P->order, P->ntickets);
+  for (size_t w = 0; w + 1 < P->wave_ptr.size(); ++w) {
+    for (int64_t t = P->wave_ptr[w]; t < P->wave_ptr[w + 1]; ++t) {
+      const int32_t r = ord[(size_t)t];
+      if (fused_task) {
+        V.entry(1, r);
+        V.entry(2, r);
+      } else if (t < n) {
+        V.entry(1, r);
+      } else {
+        V.entry(2, c == 8 ? n - 1 - r : r);
+      }
+      V.end_w();
+    }
+    V.end_s();
+  }
+}
+
+} // namespace
+
+sfg_status sfg_get_partitioning(sfg_plan* P, int32_t* nspart, int64_t* nwpart,
+                                int64_t* nentries, int64_t* s_ptr, int64_t* w_ptr,
+                                uint8_t* tags, int32_t* iters) {
+  if (!P)
+    return SFG_ERR_INVALID_ARGUMENT;
+  if (!P->inspected)
+    return set_err(P, SFG_ERR_LOGIC, "sfg_inspect has not run");
+  return guarded(P, [&] {
+    DeviceScope ds(P->device);
+    Partition V;
+    build_partition(P, V);
+    if (nspart)
+      *nspart = (int32_t)V.s_ptr.size() - 1;
+    if (nwpart)
+      *nwpart = (int64_t)V.w_ptr.size() - 1;
+    if (nentries)
+      *nentries = (int64_t)V.tags.size();
+    if (s_ptr)
+      std::copy(V.s_ptr.begin(), V.s_ptr.end(), s_ptr);
+    if (w_ptr)
+      std::copy(V.w_ptr.begin(), V.w_ptr.end(), w_ptr);
+    if (tags)
+      std::copy(V.tags.begin(), V.tags.end(), tags);
+    if (iters)
+      std::copy(V.iters.begin(), V.iters.end(), iters);
+    return SFG_OK;
+  });
+}
+
 sfg_status sfg_execute_fused(sfg_plan* P) {
   if (!P)
     return SFG_ERR_INVALID_ARGUMENT;

@@ -107,6 +107,12 @@ int main(int argc, char** argv) {
       orc_free_dag(&wj);
       orc_free_interdep(&wf);
     }
+    const sf::FusedPartitioning V = sf::fused_partitioning(st);
+    int64_t entries = 0;
+    for (const auto& sp : V.spartitions)
+      for (const auto& wp : sp)
+        entries += (int64_t)wp.size();
+    CHECK(V.b() > 0 && entries == 2 * (int64_t)M.nrows);
     const sf::FusedSchedule sched = sf::make_fused_schedule(st, 8);
     CHECK((int64_t)sched.tags.size() == 2 * (int64_t)M.nrows);
     int eidx = 0;

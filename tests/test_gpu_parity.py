@@ -349,3 +349,35 @@ def test_mline_executor_vs_oracle(orc, monkeypatch, nsys):
             Ms = Csc(n, M.colptr, M.rowidx, vals[s * nnz:(s + 1) * nnz])
             want = orc.run_sequential(combo, Ms, 7, vin=vin[s * n:(s + 1) * n])
             assert np.array_equal(got[s], want)
+
+
+# ---- the GPU schedule checked by the reference's own validator ------------------
+def _validated_by_reference(st, combo, Mo):
+    from oracle.oracle import Reference
+    part = st.partitioning()
+    assert part.w_ptr[-1] == len(part.tags)
+    rs = Reference().state(combo, Mo, 7)
+    nbad, msg = rs.validate_partitioning(part.s_ptr, part.w_ptr, part.tags, part.iters)
+    assert nbad == 0, msg
+    return part
+
+
+@pytest.mark.parametrize("name", GOLDEN_MATS)
+@pytest.mark.parametrize("combo", (1, 2, 3, 4, 5, 6, 7))
+def test_partitioning_valid_for_reference(golden, name, combo):
+    # validate_fused_partitioning (msp.hpp:1108-1237): coverage, order inside
+    # w-partitions, cross-partition dependences -- of the GPU-built schedule
+    Mo = golden_matrix(golden, name)
+    st = sf.make_state(combo, as_sf(Mo)).inspect()
+    _validated_by_reference(st, combo, Mo)
+
+
+@pytest.mark.parametrize("executor", ("chain", "mline", "levels"))
+@pytest.mark.parametrize("combo", (1, 4))
+def test_partitioning_valid_all_executors(monkeypatch, executor, combo):
+    monkeypatch.setenv("SFG_EXECUTOR", executor)
+    M = sf.config_matrix(1, size=40) if combo == 4 else sf.config_matrix(5, size=10)
+    Mo = Csc(M.n, M.colptr, M.rowidx, M.values)
+    st = sf.make_state(combo, M).inspect()
+    part = _validated_by_reference(st, combo, Mo)
+    assert part.b() > 1

@@ -142,3 +142,22 @@ def test_random_sweep_vs_live_reference(orc, seed):
     for combo in ALL_COMBOS:
         want = ref.state(combo, M, seed).execute(0)
         assert np.array_equal(orc.run_sequential(combo, M, seed), want)
+
+
+@pytest.mark.skipif(not Reference.available(), reason="reference tree not built here")
+def test_reference_partitioning_validator_is_discriminating(golden):
+    # the validator the GPU schedule is checked with (msp.hpp:1108-1237)
+    # accepts a level-ordered partitioning and rejects a reversed one
+    from conftest import golden_matrix
+    Mo = golden_matrix(golden, "grid6")
+    ref = Reference()
+    rs = ref.state(1, Mo, 7)
+    tags, iters, lp = rs.wavefront()
+    # one w-partition per entry, one s-partition per wavefront level
+    s_ptr = np.asarray(lp, np.int64)
+    w_ptr = np.arange(len(tags) + 1, dtype=np.int64)
+    nbad, msg = rs.validate_partitioning(s_ptr, w_ptr, tags, iters)
+    assert nbad == 0, msg
+    nbad, msg = rs.validate_partitioning(np.array([0, 1]), np.array([0, len(tags)]),
+                                         tags[::-1], iters[::-1])
+    assert nbad > 0 and "unsatisfied" in msg
