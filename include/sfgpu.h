@@ -145,6 +145,17 @@ sfg_status sfg_get_partitioning(sfg_plan* plan, int32_t* nspart, int64_t* nwpart
 sfg_status sfg_execute_fused(sfg_plan* plan);
 /* Unfused comparator: kernel 1 in one launch, kernel 2 in a second launch. */
 sfg_status sfg_execute_unfused(sfg_plan* plan);
+/* nsteps executions with new input vectors -- equivalent to nsteps rounds of
+ * sfg_set_vin + sfg_execute_fused + sfg_collect_outputs -- with the
+ * transfers overlapped with compute: step k+1's input is copied in and step
+ * k-1's outputs copied out while step k runs (two copy engines).  vin_host[k]
+ * holds nsys*n doubles, out_host[k] nsys*output_len doubles (the
+ * collect_outputs layout); page-locked host memory (sfg_host_alloc) is needed
+ * for the overlap.  Returns when every output is in host memory;
+ * SFG_ERR_FACTORIZATION if any step broke down.  Not for combos 3 and 7 (no
+ * input vector). */
+sfg_status sfg_execute_batch(sfg_plan* plan, int32_t nsteps, const double* const* vin_host,
+                             double* const* out_host);
 /* Waits for the plan stream; returns SFG_ERR_FACTORIZATION on breakdown. */
 sfg_status sfg_synchronize(sfg_plan* plan);
 /* collect_outputs (kernels.hpp:585-608) for every system, system-major,

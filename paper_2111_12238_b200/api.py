@@ -309,6 +309,25 @@ class KernelState:
         if sync:
             self.synchronize()
 
+    def execute_batch(self, vins, outs):
+        """len(vins) executions with new input vectors, transfers overlapped
+        with compute (sfg_execute_batch); vins[k] / outs[k] are host arrays
+        (page-locked for the overlap) of nsys*n and nsys*output_len doubles."""
+        if not self.inspected:
+            self.inspect()
+        k = len(vins)
+        if len(outs) != k:
+            raise ValueError("one output buffer per input")
+        for v in vins:
+            if v.dtype != np.float64 or v.size != self.n * self.nsys or not v.flags.c_contiguous:
+                raise ValueError("vin must be contiguous float64 of nsys * n")
+        for o in outs:
+            if o.dtype != np.float64 or o.size < self.output_len * self.nsys or not o.flags.c_contiguous:
+                raise ValueError("out must be contiguous float64 of nsys * output_len")
+        vp = (C.c_void_p * max(k, 1))(*[v.ctypes.data for v in vins])
+        op = (C.c_void_p * max(k, 1))(*[o.ctypes.data for o in outs])
+        self._chk(self.L.sfg_execute_batch(self.h, k, vp, op), "execute_batch")
+
     def execute_unfused(self, sync: bool = True):
         if not self.inspected:
             self.inspect()

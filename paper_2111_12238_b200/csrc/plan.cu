@@ -84,6 +84,11 @@ struct sfg_plan {
   int32_t trace_tiles = 0;
 
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  // sfg_execute_batch: copy streams, double-buffered host-facing staging
+  cudaStream_t copy_in = nullptr, copy_out = nullptr;
+  DBuf<double> in_stage[2], out_stage[2];
+  DBuf<unsigned long long> err_hist;
+  cudaEvent_t bev[8] = {};
   bool timed = false;
 
   // last error
@@ -1072,10 +1077,7 @@ const char* ferr_text(int kind) {
   }
 }
 
-sfg_status check_error_word(sfg_plan* P) {
-  unsigned long long key = ~0ull;
-  SFG_CUDA(cudaMemcpyAsync(&key, P->err.p, sizeof(key), cudaMemcpyDeviceToHost, P->stream));
-  SFG_CUDA(cudaStreamSynchronize(P->stream));
+sfg_status decode_error_key(sfg_plan* P, unsigned long long key) {
   if (key == ~0ull)
     return SFG_OK;
   const int kernel = (int)(key >> 62) + 1;
@@ -1084,6 +1086,42 @@ sfg_status check_error_word(sfg_plan* P) {
   return set_err(P, SFG_ERR_FACTORIZATION,
                  std::string(ferr_text(kind)) + " at index " + std::to_string(index), kind,
                  index);
+}
+
+sfg_status check_error_word(sfg_plan* P) {
+  unsigned long long key = ~0ull;
+  SFG_CUDA(cudaMemcpyAsync(&key, P->err.p, sizeof(key), cudaMemcpyDeviceToHost, P->stream));
+  SFG_CUDA(cudaStreamSynchronize(P->stream));
+  return decode_error_key(P, key);
+}
+
+// collect_outputs (kernels.hpp:585-608) of every system into a device buffer
+// in the host-facing layout (system-major), on the plan stream.
+void collect_to_device(sfg_plan* P, double* dst) {
+  const int c = P->combo;
+  const int32_t n = P->n, S = P->nsys;
+  cudaStream_t s = P->stream;
+  if (n == 0)
+    return;
+  if (c == 1 || c == 2 || c == 4 || c == 8) {
+    if (S == 1) {
+      SFG_CUDA(cudaMemcpyAsync(dst, P->vmid.p, sizeof(double) * (size_t)n,
+                               cudaMemcpyDeviceToDevice, s));
+      SFG_CUDA(cudaMemcpyAsync(dst + n, P->vout.p, sizeof(double) * (size_t)n,
+                               cudaMemcpyDeviceToDevice, s));
+    } else {
+      collect_pair_kernel<<<grid_for((int64_t)n * S), 256, 0, s>>>(P->vmid.p, P->vout.p, n, S,
+                                                                   dst);
+      count_launch();
+    }
+  } else {
+    if (P->nnzF)
+      SFG_CUDA(cudaMemcpyAsync(dst, P->fac.p, sizeof(double) * (size_t)P->nnzF,
+                               cudaMemcpyDeviceToDevice, s));
+    const double* tail = (c == 7 || c == 3) ? P->dvec.p : P->vout.p;
+    SFG_CUDA(cudaMemcpyAsync(dst + P->nnzF, tail, sizeof(double) * (size_t)n,
+                             cudaMemcpyDeviceToDevice, s));
+  }
 }
 
 // One fused execution: re-initialise outputs + ticket counter + error word,
@@ -1370,6 +1408,13 @@ sfg_status sfg_plan_destroy(sfg_plan* P) {
     for (auto& e : P->ev)
       if (e)
         cudaEventDestroy(e);
+    for (auto& e : P->bev)
+      if (e)
+        cudaEventDestroy(e);
+    if (P->copy_in)
+      cudaStreamDestroy(P->copy_in);
+    if (P->copy_out)
+      cudaStreamDestroy(P->copy_out);
     if (P->own_stream)
       cudaStreamDestroy(P->own_stream);
   }
@@ -1954,6 +1999,88 @@ sfg_status sfg_get_partitioning(sfg_plan* P, int32_t* nspart, int64_t* nwpart,
       std::copy(V.tags.begin(), V.tags.end(), tags);
     if (iters)
       std::copy(V.iters.begin(), V.iters.end(), iters);
+    return SFG_OK;
+  });
+}
+
+// K executions with new right-hand sides, transfers overlapped with compute:
+// the input of step k+1 streams in (copy engine 1) and the outputs of step
+// k-1 stream out (copy engine 2) while step k runs.  Each step's error word
+// is kept, so a breakdown in any step is reported like sfg_synchronize would.
+sfg_status sfg_execute_batch(sfg_plan* P, int32_t nsteps, const double* const* vin_host,
+                             double* const* out_host) {
+  if (!P || nsteps < 0 || (nsteps > 0 && (!vin_host || !out_host)) || P->combo == 3 ||
+      P->combo == 7)
+    return SFG_ERR_INVALID_ARGUMENT;
+  if (!P->inspected)
+    return set_err(P, SFG_ERR_LOGIC, "sfg_inspect has not run");
+  return guarded(P, [&] {
+    DeviceScope ds(P->device);
+    LaunchScope ls(P);
+    if (nsteps == 0)
+      return SFG_OK;
+    const int32_t n = P->n, S = P->nsys;
+    const int64_t nv = (int64_t)n * S;
+    const int c = P->combo;
+    const int64_t olen = ((c == 1 || c == 2 || c == 4 || c == 8) ? 2 * (int64_t)n : P->nnzF + n) * S;
+    if (!P->copy_in) {
+      SFG_CUDA(cudaStreamCreateWithFlags(&P->copy_in, cudaStreamNonBlocking));
+      SFG_CUDA(cudaStreamCreateWithFlags(&P->copy_out, cudaStreamNonBlocking));
+      for (auto& e : P->bev)
+        SFG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
+    for (int b = 0; b < 2; ++b) {
+      if (P->in_stage[b].n < nv)
+        P->in_stage[b].alloc(std::max<int64_t>(nv, 1));
+      if (P->out_stage[b].n < olen)
+        P->out_stage[b].alloc(std::max<int64_t>(olen, 1));
+    }
+    if (P->err_hist.n < nsteps)
+      P->err_hist.alloc(nsteps);
+    cudaEvent_t* in_ready = P->bev;      // [2]
+    cudaEvent_t* in_free = P->bev + 2;   // [2]
+    cudaEvent_t* out_ready = P->bev + 4; // [2]
+    cudaEvent_t* out_free = P->bev + 6;  // [2]
+    // start with every staging buffer free
+    for (int b = 0; b < 2; ++b) {
+      SFG_CUDA(cudaEventRecord(in_free[b], P->stream));
+      SFG_CUDA(cudaEventRecord(out_free[b], P->stream));
+    }
+    auto stage_in = [&](int32_t k) {
+      const int b = k & 1;
+      SFG_CUDA(cudaStreamWaitEvent(P->copy_in, in_free[b], 0));
+      SFG_CUDA(cudaMemcpyAsync(P->in_stage[b].p, vin_host[k], sizeof(double) * (size_t)nv,
+                               cudaMemcpyHostToDevice, P->copy_in));
+      SFG_CUDA(cudaEventRecord(in_ready[b], P->copy_in));
+    };
+    stage_in(0);
+    for (int32_t k = 0; k < nsteps; ++k) {
+      const int b = k & 1;
+      if (k + 1 < nsteps)
+        stage_in(k + 1);
+      SFG_CUDA(cudaStreamWaitEvent(P->stream, in_ready[b], 0));
+      interleave(P->in_stage[b].p, n, S, P->vin.p, P->stream);
+      SFG_CUDA(cudaEventRecord(in_free[b], P->stream));
+      exec_fused_impl(P, P->ev[1], P->ev[2]);
+      SFG_CUDA(cudaMemcpyAsync(P->err_hist.p + k, P->err.p, sizeof(unsigned long long),
+                               cudaMemcpyDeviceToDevice, P->stream));
+      SFG_CUDA(cudaStreamWaitEvent(P->stream, out_free[b], 0));
+      collect_to_device(P, P->out_stage[b].p);
+      SFG_CUDA(cudaEventRecord(out_ready[b], P->stream));
+      SFG_CUDA(cudaStreamWaitEvent(P->copy_out, out_ready[b], 0));
+      SFG_CUDA(cudaMemcpyAsync(out_host[k], P->out_stage[b].p, sizeof(double) * (size_t)olen,
+                               cudaMemcpyDeviceToHost, P->copy_out));
+      SFG_CUDA(cudaEventRecord(out_free[b], P->copy_out));
+    }
+    SFG_CUDA(cudaStreamSynchronize(P->copy_out));
+    SFG_CUDA(cudaStreamSynchronize(P->stream));
+    std::vector<unsigned long long> eh((size_t)nsteps);
+    SFG_CUDA(cudaMemcpy(eh.data(), P->err_hist.p, sizeof(unsigned long long) * eh.size(),
+                        cudaMemcpyDeviceToHost));
+    for (unsigned long long key : eh)
+      if (key != ~0ull)
+        return decode_error_key(P, key);
+    P->timed = false;
     return SFG_OK;
   });
 }

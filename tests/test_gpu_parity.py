@@ -381,3 +381,44 @@ def test_partitioning_valid_all_executors(monkeypatch, executor, combo):
     st = sf.make_state(combo, M).inspect()
     part = _validated_by_reference(st, combo, Mo)
     assert part.b() > 1
+
+
+# ---- batched executions with overlapped transfers (sfg_execute_batch) ----------
+@pytest.mark.parametrize("combo,nsys", ((8, 8), (1, 2), (4, 1), (2, 1), (5, 1), (6, 1)))
+def test_execute_batch_equals_serial(orc, combo, nsys):
+    from paper_2111_12238_b200 import abi
+    if combo in (1, 8):
+        M, vals = sf.config5_systems(size=12, nsys=nsys)
+    else:
+        M, vals = sf.config_matrix({4: 1, 2: 1, 5: 2, 6: 3}[combo], size=16), None
+    n = M.n
+    st = sf.make_state(combo, M, nsys=nsys, values=vals).inspect()
+    K = 5
+    rng = np.random.default_rng(combo)
+    ins = [abi.PinnedArray(nsys * n) for _ in range(K)]
+    outs = [abi.PinnedArray(nsys * st.output_len) for _ in range(K)]
+    for a in ins:
+        a.array[:] = rng.uniform(-1, 1, nsys * n)
+    st.execute_batch([a.array for a in ins], [o.array for o in outs])
+    for k in range(K):
+        st.set_vin(ins[k].array)
+        st.execute_fused()
+        assert np.array_equal(outs[k].array, st.collect_outputs())
+    for a in ins + outs:
+        a.free()
+
+
+def test_execute_batch_reports_breakdown(golden):
+    from paper_2111_12238_b200 import abi
+    cp = golden["breakdown/colptr"]
+    M = sf.CscMatrix(len(cp) - 1, cp, golden["breakdown/rowidx"], golden["breakdown/values"])
+    st = sf.make_state(5, M, seed=1).inspect()
+    ins = [abi.PinnedArray(M.n) for _ in range(3)]
+    outs = [abi.PinnedArray(st.output_len) for _ in range(3)]
+    for a in ins:
+        a.array[:] = 1.0
+    with pytest.raises(sf.FactorizationError) as e:
+        st.execute_batch([a.array for a in ins], [o.array for o in outs])
+    assert e.value.index == 7
+    for a in ins + outs:
+        a.free()
