@@ -54,6 +54,9 @@ struct EllArgs {
   double* vout = nullptr; // n + 1 rows (row n all zero)
   int warps_per_cta = 4;
   int blocks_per_sm = 0;
+  int ws_slots = 3; // warp-specialised executor: slots per warp pair (2 or 3)
+  int ws_pairs = 2; // warp pairs per CTA (more CTAs per SM fit when small)
+  int ws_fence = 0; // diagnostics: fence after each tile's publishes
   // diagnostics: completion time (globaltimer ns) of tile u of work item i
   // at trace[i * trace_tiles + u]; null in production
   unsigned long long* trace = nullptr;
@@ -64,5 +67,9 @@ struct EllArgs {
 constexpr int32_t kEllMaxWidth = 16;
 
 void launch_chain_ell(const EllArgs& a, int32_t CHN, cudaStream_t s);
+
+// Warp-specialised variant (chainws.cu): a loader warp and a compute warp per
+// chain share a ring of shared-memory slots.  Combo 8, S in {4, 8, 16, 32}.
+void launch_chain_ws(const EllArgs& a, int32_t CHN, cudaStream_t s);
 
 } // namespace sfg

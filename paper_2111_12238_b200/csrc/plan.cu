@@ -69,6 +69,7 @@ struct sfg_plan {
   bool use_chain = false;
   ChainLayout ch_f, ch_b;
   bool use_ell = false; // TMA-staged chain-ELL executor (batched combo 8)
+  bool use_ws = false;  // warp-specialised chain-ELL executor (batched combo 8)
   EllLayout ell_f, ell_b;
   int32_t ell_chn = 0;
   DBuf<int32_t> tail_ptr, tail_rows;
@@ -723,7 +724,8 @@ void do_inspect(sfg_plan* P) {
     if (combo == 4)
       build_tails(P->ch_f, P->ar_ptr.p, P->ar_idx.p, n, P->tail_ptr, P->tail_rows, s);
     const char* ell_env = getenv("SFG_ELL");
-    if (combo == 8 && P->nsys >= 2 && ell_env && std::string(ell_env) == "1") {
+    const bool want_ws = ex && std::string(ex) == "ws" && combo == 8 && P->nsys >= 4;
+    if (combo == 8 && P->nsys >= 2 && ((ell_env && std::string(ell_env) == "1") || want_ws)) {
       const int32_t w = std::max(ell_width(P->lr_ptr.p, P->lr_idx.p, n, +1, P->ch_f, s),
                                  ell_width(P->lt_ptr.p, P->lt_idx.p, n, -1, P->ch_b, s));
       const int32_t chn = std::max(4, (w + 3) / 4 * 4);
@@ -731,7 +733,8 @@ void do_inspect(sfg_plan* P) {
         P->ell_chn = chn;
         build_ell(P->lr_ptr.p, P->lr_idx.p, P->lr_val.p, n, P->nsys, +1, chn, P->ch_f, P->ell_f, s);
         build_ell(P->lt_ptr.p, P->lt_idx.p, P->lt_val.p, n, P->nsys, -1, chn, P->ch_b, P->ell_b, s);
-        P->use_ell = true;
+        P->use_ell = !want_ws;
+        P->use_ws = want_ws;
       }
     }
     if (getenv("SFG_TRACE")) {
@@ -750,6 +753,12 @@ EllArgs ell_args(sfg_plan* P) {
   EllArgs a;
   a.n = P->n;
   a.S = P->nsys;
+  if (const char* e = getenv("SFG_WS_SLOTS"))
+    a.ws_slots = atoi(e);
+  if (const char* e = getenv("SFG_WS_PAIRS"))
+    a.ws_pairs = atoi(e);
+  if (const char* e = getenv("SFG_WS_FENCE"))
+    a.ws_fence = atoi(e);
   a.counter = P->counter.p;
   a.err = P->err.p;
   a.f_cstart = P->ch_f.cstart.p;
@@ -1152,7 +1161,12 @@ void exec_fused_impl(sfg_plan* P, cudaEvent_t kb, cudaEvent_t ke) {
   }
   launch_prep(r, nr, P->counter.p, P->err.p, P->stream);
   SFG_CUDA(cudaEventRecord(kb, P->stream));
-  if (P->use_ell) {
+  if (P->use_ws) {
+    EllArgs e = ell_args(P);
+    e.seg_begin = 0;
+    e.seg_end = P->ch_f.nbatch + P->ch_b.nbatch;
+    launch_chain_ws(e, P->ell_chn, P->stream);
+  } else if (P->use_ell) {
     EllArgs e = ell_args(P);
     e.seg_begin = 0;
     e.seg_end = P->ch_f.nbatch + P->ch_b.nbatch;
@@ -1193,16 +1207,22 @@ void exec_unfused_impl(sfg_plan* P, cudaEvent_t kb, cudaEvent_t ke) {
     r1[n1++] = {P->fac.p, P->nnzF};
   launch_prep(r1, n1, P->counter.p, P->err.p, P->stream);
   SFG_CUDA(cudaEventRecord(kb, P->stream));
-  if (P->use_ell) {
+  if (P->use_ell || P->use_ws) {
     EllArgs e = ell_args(P);
+    auto launch = [&](const EllArgs& x) {
+      if (P->use_ws)
+        launch_chain_ws(x, P->ell_chn, P->stream);
+      else
+        launch_chain_ell(x, P->ell_chn, P->stream);
+    };
     e.seg_begin = 0;
     e.seg_end = P->ch_f.nbatch;
-    launch_chain_ell(e, P->ell_chn, P->stream);
+    launch(e);
     FillRegion r2[1] = {{P->vout.p, nv}};
     launch_prep(r2, 1, P->counter.p, nullptr, P->stream);
     e.seg_begin = P->ch_f.nbatch;
     e.seg_end = P->ch_f.nbatch + P->ch_b.nbatch;
-    launch_chain_ell(e, P->ell_chn, P->stream);
+    launch(e);
     SFG_CUDA(cudaEventRecord(ke, P->stream));
     return;
   }
@@ -1535,7 +1555,7 @@ sfg_status sfg_set_values(sfg_plan* P, const double* values_host) {
     }
     if (c == 7)
       dscal_vector(P->lc_ptr.p, P->lc_val.p, n, P->dvec.p, s);
-    if (P->use_ell) { // the chain-ELL records hold copies of the values
+    if (P->use_ell || P->use_ws) { // the chain-ELL records hold copies of the values
       build_ell(P->lr_ptr.p, P->lr_idx.p, P->lr_val.p, n, S, +1, P->ell_chn, P->ch_f, P->ell_f, s);
       build_ell(P->lt_ptr.p, P->lt_idx.p, P->lt_val.p, n, S, -1, P->ell_chn, P->ch_b, P->ell_b, s);
     }

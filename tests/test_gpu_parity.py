@@ -335,9 +335,10 @@ def test_alternative_executors_golden(golden, monkeypatch, executor, name):
         _check_linear_extension(st, st.dag(3))
 
 
-@pytest.mark.parametrize("nsys", (1, 2, 8, 32))
-def test_mline_executor_vs_oracle(orc, monkeypatch, nsys):
-    monkeypatch.setenv("SFG_EXECUTOR", "mline")
+@pytest.mark.parametrize("executor,nsys", (("mline", 1), ("mline", 2), ("mline", 8), ("mline", 32),
+                                            ("ws", 4), ("ws", 8), ("ws", 16), ("ws", 32)))
+def test_mline_executor_vs_oracle(orc, monkeypatch, executor, nsys):
+    monkeypatch.setenv("SFG_EXECUTOR", executor)
     M, vals = sf.config5_systems(size=24, nsys=nsys)
     n, nnz = M.n, M.nnz
     vin = np.concatenate([sf.gen_vector(n, 7 + s) for s in range(nsys)])
