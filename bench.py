@@ -414,7 +414,11 @@ def other_configs(args):
                "achieved_gbs": byts / (ker / 1e3) / 1e9,
                "frac": byts / (ker / 1e3) / 1e9 / peak,
                "unfused_ms_per_exec": ut / reps, "fused_speedup": (ut / reps) / ms,
-               "critical_path": int(st.schedule().nspartitions())}
+               # level_info(joint_dag) (dag.hpp:197-218) and the executor's own
+               # dependency levels (s-partitions of its FusedPartitioning)
+               "critical_path": int(st.level_info(3).critical_path),
+               "executor_levels": int(st.partitioning().b()),
+               "traffic": ncu_traffic(f"config{cfg}")}
         if Reference.available() and not args.no_cpu_baseline:
             try:
                 r = reference_fused(cfg, M, None, vin, T, warmups=1, repeats=3)
