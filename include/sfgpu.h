@@ -44,7 +44,8 @@ typedef enum {
   SFG_ERR_INVALID_ARGUMENT = 3, /* std::invalid_argument (kernels.hpp:72, msp.hpp:828-829) */
   SFG_ERR_CUDA = 4,             /* CUDA runtime failure (no reference analogue) */
   SFG_ERR_LOGIC = 5,            /* std::logic_error (executor.hpp:398-399) */
-  SFG_ERR_NO_DEVICE = 6         /* no CUDA device: the library never falls back to the CPU */
+  SFG_ERR_NO_DEVICE = 6,        /* no CUDA device: the library never falls back to the CPU */
+  SFG_ERR_PARSE = 7             /* sparsefuse::ParseError (types.hpp:33-36): file input */
 } sfg_status;
 
 /* Factorization error kinds reported by sfg_last_error (same numbering as
@@ -212,6 +213,20 @@ sfg_status sfg_matrix_free(sfg_matrix* m);
  * (mt19937_64 seeded seed0 + s) to diagonal entry i.  out: nsys*nnz doubles. */
 sfg_status sfg_matrix_perturb_diag(const sfg_matrix* m, int32_t nsys,
                                    uint64_t seed0, double* out);
+/* Matrix Market input/output (matrix_market.hpp:59-152): coordinate real,
+ * general or symmetric (expanded), 1-based, duplicates summed; square only.
+ * Errors: SFG_ERR_PARSE / SFG_ERR_INVALID_MATRIX with the message in msg. */
+sfg_status sfg_matrix_read_mm(const char* path, sfg_matrix** out, char* msg, int32_t msg_len);
+sfg_status sfg_matrix_write_mm(const sfg_matrix* m, const char* path);
+/* Wrap host CSC arrays (copied) as a matrix handle. */
+sfg_status sfg_matrix_from_csc(int32_t n, const int32_t* colptr, const int32_t* rowidx,
+                               const double* values, sfg_matrix** out);
+/* B = P A P^T with row/column i of A becoming perm[i] of B
+ * (permute_symmetric, matrix.hpp:135-173); SFG_ERR_INVALID_MATRIX if perm is
+ * not a permutation.  read_permutation (matrix_market.hpp:140-152): one
+ * 0-based index per line, exactly n of them. */
+sfg_status sfg_matrix_permute(const sfg_matrix* m, const int32_t* perm, sfg_matrix** out);
+sfg_status sfg_read_permutation(const char* path, int32_t n, int32_t* perm);
 /* gen_vector (fixtures.hpp:148-155). */
 sfg_status sfg_gen_vector(int32_t n, uint64_t seed, double* out);
 

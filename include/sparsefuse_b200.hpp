@@ -65,6 +65,12 @@ public:
   using std::runtime_error::runtime_error;
 };
 
+// types.hpp:33-36
+class ParseError : public std::runtime_error {
+public:
+  using std::runtime_error::runtime_error;
+};
+
 // matrix.hpp:18-27
 struct CscMatrix {
   Index nrows = 0;
@@ -443,6 +449,62 @@ inline std::vector<double> collect_outputs(KernelState& st) {
                 sfg_collect_outputs(st.handle(), out.data(), (std::int64_t)out.size()),
                 "collect_outputs");
   return out;
+}
+
+namespace detail {
+inline CscMatrix from_handle(sfg_matrix* h) {
+  CscMatrix M;
+  std::int32_t n = 0;
+  std::int64_t nnz = 0;
+  sfg_matrix_dims(h, &n, &nnz);
+  M.nrows = M.ncols = n;
+  M.colptr.resize((size_t)n + 1);
+  M.rowidx.resize((size_t)nnz);
+  M.values.resize((size_t)nnz);
+  sfg_matrix_copy(h, M.colptr.data(), M.rowidx.data(), M.values.data());
+  sfg_matrix_free(h);
+  return M;
+}
+} // namespace detail
+
+// matrix_market.hpp:59-121 (coordinate real, general/symmetric; square)
+inline CscMatrix read_matrix_market(const std::string& path) {
+  sfg_matrix* h = nullptr;
+  char msg[512] = {0};
+  const sfg_status st = sfg_matrix_read_mm(path.c_str(), &h, msg, (std::int32_t)sizeof(msg));
+  if (st == SFG_ERR_INVALID_MATRIX)
+    throw InvalidMatrixError(msg);
+  if (st != SFG_OK)
+    throw ParseError(msg[0] ? msg : ("cannot read " + path).c_str());
+  return detail::from_handle(h);
+}
+
+// matrix_market.hpp:123-138
+inline void write_matrix_market(const CscMatrix& A, const std::string& path) {
+  sfg_matrix* h = nullptr;
+  if (sfg_matrix_from_csc(A.ncols, A.colptr.data(), A.rowidx.data(), A.values.data(), &h) !=
+      SFG_OK)
+    throw std::invalid_argument("bad CSC arrays");
+  const sfg_status st = sfg_matrix_write_mm(h, path.c_str());
+  sfg_matrix_free(h);
+  if (st != SFG_OK)
+    throw ParseError("write failed for " + path);
+}
+
+// matrix.hpp:135-173: B = P A P^T, row/column i of A -> perm[i] of B
+inline CscMatrix permute_symmetric(const CscMatrix& A, const std::vector<Index>& perm) {
+  if (A.nrows != A.ncols || (Index)perm.size() != A.ncols)
+    throw InvalidMatrixError("permutation length mismatch");
+  sfg_matrix* h = nullptr;
+  if (sfg_matrix_from_csc(A.ncols, A.colptr.data(), A.rowidx.data(), A.values.data(), &h) !=
+      SFG_OK)
+    throw std::invalid_argument("bad CSC arrays");
+  sfg_matrix* out = nullptr;
+  const sfg_status st = sfg_matrix_permute(h, perm.data(), &out);
+  sfg_matrix_free(h);
+  if (st != SFG_OK)
+    throw InvalidMatrixError("not a permutation");
+  return detail::from_handle(out);
 }
 
 // fixtures.hpp:148-155

@@ -294,6 +294,8 @@ class Reference:
         L.ref_validate_partitioning.argtypes = [vp, C.c_int32, _i64p, _i64p,
                                                 C.POINTER(C.c_uint8), _i32p, C.c_char_p, C.c_int]
         L.ref_validate_partitioning.restype = C.c_int64
+        L.ref_read_mm.argtypes = [C.c_char_p, C.c_char_p, C.c_int]
+        L.ref_read_mm.restype = vp
         self.lib = L
 
     # ---- fixtures.hpp
@@ -315,6 +317,40 @@ class Reference:
         self.lib.ref_mat_copy(h, _p(cp, _i32p), _p(ri, _i32p), _p(va, _f64p))
         self.lib.ref_mat_free(h)
         return Csc(n.value, cp, ri[:nnz.value], va[:nnz.value])
+
+    def read_matrix_market(self, path: str) -> Csc:
+        """The reference's read_matrix_market (matrix_market.hpp:59-121).
+        Runs in a child interpreter without numpy: the reference's iostream
+        parsing crashed in a process that had imported numpy (not analysed
+        further -- test infrastructure only)."""
+        import json
+        import subprocess
+        import sys
+        code = (
+            "import ctypes as C, json, sys\n"
+            f"L = C.CDLL({self.PATH!r})\n"
+            "L.ref_read_mm.argtypes = [C.c_char_p, C.c_char_p, C.c_int]\n"
+            "L.ref_read_mm.restype = C.c_void_p\n"
+            "L.ref_mat_dims.argtypes = [C.c_void_p, C.POINTER(C.c_int32), C.POINTER(C.c_int32)]\n"
+            "L.ref_mat_copy.argtypes = [C.c_void_p, C.POINTER(C.c_int32), C.POINTER(C.c_int32), C.POINTER(C.c_double)]\n"
+            "msg = C.create_string_buffer(512)\n"
+            "h = L.ref_read_mm(sys.argv[1].encode(), msg, 512)\n"
+            "if not h:\n"
+            "    print(json.dumps({'error': msg.value.decode()})); sys.exit(0)\n"
+            "n = C.c_int32(); nnz = C.c_int32()\n"
+            "L.ref_mat_dims(h, C.byref(n), C.byref(nnz))\n"
+            "cp = (C.c_int32 * (n.value + 1))(); ri = (C.c_int32 * max(nnz.value, 1))()\n"
+            "va = (C.c_double * max(nnz.value, 1))()\n"
+            "L.ref_mat_copy(h, cp, ri, va)\n"
+            "print(json.dumps({'n': n.value, 'cp': list(cp), 'ri': list(ri)[:nnz.value],"
+            " 'va': [v.hex() for v in list(va)[:nnz.value]]}))\n")
+        r = subprocess.run([sys.executable, "-c", code, path], capture_output=True, text=True,
+                           check=True)
+        d = json.loads(r.stdout)
+        if "error" in d:
+            raise ValueError(d["error"])
+        return Csc(d["n"], np.array(d["cp"], np.int32), np.array(d["ri"], np.int32),
+                   np.array([float.fromhex(v) for v in d["va"]], np.float64))
 
     def gen_grid_laplacian(self, k: int) -> Csc:
         return self._mat(0, k)

@@ -13,6 +13,7 @@
 #include <sparsefuse/fixtures.hpp>
 #include <sparsefuse/kernels.hpp>
 #include <sparsefuse/lbc.hpp>
+#include <sparsefuse/matrix_market.hpp>
 #include <sparsefuse/msp.hpp>
 
 #include "fixture11.hpp"
@@ -382,6 +383,16 @@ int64_t ref_validate_partitioning(void* s, int32_t nspart, const int64_t* s_ptr,
   if (!bad.empty())
     put_msg(msg, ml, bad.front() + " (" + std::to_string(bad.size()) + " violations)");
   return (int64_t)bad.size();
+}
+
+// read_matrix_market (matrix_market.hpp:59-121); nullptr + message on error.
+void* ref_read_mm(const char* path, char* msg, int ml) {
+  try {
+    return new CscMatrix(read_matrix_market(path));
+  } catch (const std::exception& e) {
+    put_msg(msg, ml, e.what());
+    return nullptr;
+  }
 }
 
 } // extern "C"

@@ -6,20 +6,22 @@ The compute path is libsfgpu.so (CUDA, built in-tree by ``make -C
 paper_2111_12238_b200``); this package is its Python face.  There is no CPU
 fallback.
 """
-from .api import (COMBOS, CscMatrix, DepDag, FactorizationError, FusedSchedule,
-                  InterDep, InvalidMatrixError, KernelState, LevelInfo,
-                  NoDeviceError, build_g1, build_g2, collect_outputs,
+from .api import (COMBOS, CscMatrix, DepDag, FactorizationError, FusedPartitioning,
+                  FusedSchedule, InterDep, InvalidMatrixError, KernelState, LevelInfo,
+                  NoDeviceError, ParseError, build_g1, build_g2, collect_outputs,
                   compute_reuse, config5_systems, config_matrix, execute_fused,
                   execute_unfused, gen_banded_spd, gen_grid_laplacian,
                   gen_vector, inter_dag, joint_dag, level_info,
-                  make_fused_schedule, make_state, reset)
+                  make_fused_schedule, make_state, permute_symmetric,
+                  read_matrix_market, read_permutation, reset, write_matrix_market)
 
 __all__ = [
-    "COMBOS", "CscMatrix", "DepDag", "FactorizationError", "FusedSchedule",
-    "InterDep", "InvalidMatrixError", "KernelState", "LevelInfo",
-    "NoDeviceError", "build_g1", "build_g2", "collect_outputs",
+    "COMBOS", "CscMatrix", "DepDag", "FactorizationError", "FusedPartitioning",
+    "FusedSchedule", "InterDep", "InvalidMatrixError", "KernelState", "LevelInfo",
+    "NoDeviceError", "ParseError", "build_g1", "build_g2", "collect_outputs",
     "compute_reuse", "config5_systems", "config_matrix", "execute_fused",
     "execute_unfused", "gen_banded_spd", "gen_grid_laplacian", "gen_vector",
     "inter_dag", "joint_dag", "level_info", "make_fused_schedule",
-    "make_state", "reset",
+    "make_state", "permute_symmetric", "read_matrix_market", "read_permutation",
+    "reset", "write_matrix_market",
 ]

@@ -21,6 +21,7 @@ SFG_ERR_INVALID_ARGUMENT = 3
 SFG_ERR_CUDA = 4
 SFG_ERR_LOGIC = 5
 SFG_ERR_NO_DEVICE = 6
+SFG_ERR_PARSE = 7
 
 # Every function include/sfgpu.h declares (checked by tests/test_abi.py).
 EXPORTS = (
@@ -31,7 +32,8 @@ EXPORTS = (
     "sfg_get_schedule", "sfg_get_partitioning", "sfg_execute_fused", "sfg_execute_batch", "sfg_execute_unfused",
     "sfg_synchronize", "sfg_collect_outputs", "sfg_device_output",
     "sfg_last_error", "sfg_launch_count", "sfg_last_exec_ms", "sfg_matrix_gen",
-    "sfg_matrix_dims", "sfg_matrix_copy", "sfg_matrix_free",
+    "sfg_matrix_dims", "sfg_matrix_copy", "sfg_matrix_free", "sfg_matrix_read_mm",
+    "sfg_matrix_write_mm", "sfg_matrix_from_csc", "sfg_matrix_permute", "sfg_read_permutation",
     "sfg_matrix_perturb_diag", "sfg_gen_vector",
 )
 
@@ -130,6 +132,16 @@ def load(path: str | None = None):
     L.sfg_matrix_perturb_diag.restype = st
     L.sfg_gen_vector.argtypes = [C.c_int32, C.c_uint64, f64p]
     L.sfg_gen_vector.restype = st
+    L.sfg_matrix_read_mm.argtypes = [C.c_char_p, C.POINTER(vp), C.c_char_p, C.c_int32]
+    L.sfg_matrix_read_mm.restype = st
+    L.sfg_matrix_write_mm.argtypes = [vp, C.c_char_p]
+    L.sfg_matrix_write_mm.restype = st
+    L.sfg_matrix_from_csc.argtypes = [C.c_int32, i32p, i32p, f64p, C.POINTER(vp)]
+    L.sfg_matrix_from_csc.restype = st
+    L.sfg_matrix_permute.argtypes = [vp, i32p, C.POINTER(vp)]
+    L.sfg_matrix_permute.restype = st
+    L.sfg_read_permutation.argtypes = [C.c_char_p, C.c_int32, i32p]
+    L.sfg_read_permutation.restype = st
     if path is None:
         _lib = L
     return L

@@ -437,6 +437,88 @@ def gen_vector(n: int, seed: int) -> np.ndarray:
     return out[:n]
 
 
+class ParseError(RuntimeError):
+    """types.hpp:33-36 (Matrix Market and permutation files)."""
+
+
+def _from_handle(L, h) -> CscMatrix:
+    n = C.c_int32()
+    nnz = C.c_int64()
+    L.sfg_matrix_dims(h, C.byref(n), C.byref(nnz))
+    cp = np.empty(n.value + 1, np.int32)
+    ri = np.empty(max(nnz.value, 1), np.int32)
+    va = np.empty(max(nnz.value, 1), np.float64)
+    L.sfg_matrix_copy(h, ptr(cp, i32p), ptr(ri, i32p), ptr(va, f64p))
+    return CscMatrix(n.value, cp, ri[:nnz.value], va[:nnz.value])
+
+
+def _handle(L, M: CscMatrix):
+    h = C.c_void_p()
+    cp = np.ascontiguousarray(M.colptr, np.int32)
+    ri = np.ascontiguousarray(M.rowidx, np.int32)
+    va = np.ascontiguousarray(M.values, np.float64)
+    if L.sfg_matrix_from_csc(M.n, ptr(cp, i32p), ptr(ri, i32p), ptr(va, f64p), C.byref(h)) != abi.SFG_OK:
+        raise ValueError("bad CSC arrays")
+    return h
+
+
+def read_matrix_market(path: str) -> CscMatrix:
+    """read_matrix_market (matrix_market.hpp:59-121): coordinate real,
+    general or symmetric (expanded), duplicates summed."""
+    L = abi.load()
+    h = C.c_void_p()
+    msg = C.create_string_buffer(512)
+    st = L.sfg_matrix_read_mm(path.encode(), C.byref(h), msg, 512)
+    if st == abi.SFG_ERR_PARSE:
+        raise ParseError(msg.value.decode())
+    if st == abi.SFG_ERR_INVALID_MATRIX:
+        raise InvalidMatrixError(msg.value.decode())
+    if st != abi.SFG_OK:
+        raise ValueError(msg.value.decode() or "read_matrix_market failed")
+    try:
+        return _from_handle(L, h)
+    finally:
+        L.sfg_matrix_free(h)
+
+
+def write_matrix_market(M: CscMatrix, path: str) -> None:
+    """write_matrix_market (matrix_market.hpp:123-138), round-trip exact."""
+    L = abi.load()
+    h = _handle(L, M)
+    try:
+        if L.sfg_matrix_write_mm(h, path.encode()) != abi.SFG_OK:
+            raise ParseError("cannot write " + path)
+    finally:
+        L.sfg_matrix_free(h)
+
+
+def permute_symmetric(M: CscMatrix, perm) -> CscMatrix:
+    """B = P A P^T, row/column i of A -> perm[i] of B (matrix.hpp:135-173)."""
+    L = abi.load()
+    p = np.ascontiguousarray(perm, np.int32)
+    if p.size != M.n:
+        raise InvalidMatrixError("permutation length mismatch")
+    h = _handle(L, M)
+    out = C.c_void_p()
+    try:
+        if L.sfg_matrix_permute(h, ptr(p, i32p), C.byref(out)) != abi.SFG_OK:
+            raise InvalidMatrixError("not a permutation")
+        try:
+            return _from_handle(L, out)
+        finally:
+            L.sfg_matrix_free(out)
+    finally:
+        L.sfg_matrix_free(h)
+
+
+def read_permutation(path: str, n: int) -> np.ndarray:
+    """read_permutation (matrix_market.hpp:140-152)."""
+    out = np.empty(max(n, 1), np.int32)
+    if abi.load().sfg_read_permutation(path.encode(), n, ptr(out, i32p)) != abi.SFG_OK:
+        raise ParseError(f"{path}: expected {n} permutation entries")
+    return out[:n]
+
+
 def _matrix(kind: int, a: int, b: int = 0, seed: int = 0, nsys_perturb: int = 0,
             seed0: int = 1000):
     L = abi.load()

@@ -15,12 +15,7 @@
 #include <random>
 #include <vector>
 
-struct sfg_matrix {
-  int32_t n = 0;
-  std::vector<int32_t> colptr;
-  std::vector<int32_t> rowidx;
-  std::vector<double> values;
-};
+#include "matrix_handle.hpp"
 
 namespace {
 

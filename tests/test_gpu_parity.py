@@ -423,3 +423,27 @@ def test_execute_batch_reports_breakdown(golden):
     assert e.value.index == 7
     for a in ins + outs:
         a.free()
+
+
+def test_matrix_market_input_end_to_end(orc, tmp_path):
+    # a matrix read from a Matrix Market file (symmetric storage) goes
+    # through make_state exactly like a generated one
+    M = sf.config_matrix(2, size=10)
+    lines = ["%%MatrixMarket matrix coordinate real symmetric"]
+    ent = []
+    for j in range(M.n):
+        for p in range(M.colptr[j], M.colptr[j + 1]):
+            if M.rowidx[p] >= j:
+                ent.append(f"{M.rowidx[p] + 1} {j + 1} {M.values[p]:.17g}")
+    lines.append(f"{M.n} {M.n} {len(ent)}")
+    path = tmp_path / "c2.mtx"
+    path.write_text("\n".join(lines + ent) + "\n")
+    R = sf.read_matrix_market(str(path))
+    assert np.array_equal(R.values, M.values)
+    perm = np.random.default_rng(2).permutation(R.n).astype(np.int32)
+    P = sf.permute_symmetric(R, perm)
+    for combo in (5, 6):
+        st = sf.make_state(combo, P)
+        st.execute_fused()
+        want = orc.run_sequential(combo, Csc(P.n, P.colptr, P.rowidx, P.values), 7)
+        assert np.array_equal(st.collect_outputs(), want)
