@@ -427,8 +427,32 @@ def other_configs(args):
                                         "inspector_s": r["inspector_s"]}
             except Exception as e:  # keep the bench line even if the CPU leg fails
                 rec["cpu_reference"] = {"error": str(e)[:200]}
+        # NER (bench.hpp:29-36): executions that amortise this GPU's
+        # inspection (make_state + inspect) against the CPU reference
+        t0 = time.perf_counter()
+        st2 = sf.make_state(combo, M, seed=7).inspect()
+        insp = time.perf_counter() - t0
+        st2.close()
+        rec["inspector_s"] = insp
+        cpu = rec.get("cpu_reference", {}).get("ms_per_exec")
+        if cpu:
+            rec["ner_vs_cpu_reference"] = (insp / ((cpu - ms) / 1e3)) if cpu > ms else None
         out[f"config{cfg}"] = rec
         st.close()
+    # the iterative solver the executors serve: PCG with the IC0
+    # factor (combo 5) and the fused forward/backward solve (combo 8) as M^-1
+    M = sf.config_matrix(2)
+    t0 = time.perf_counter()
+    pcg = sf.PCG(M)
+    setup = time.perf_counter() - t0
+    b = sf.gen_vector(M.n, 7)
+    pcg.solve(b, rtol=1e-10, maxit=1000)  # warm-up
+    x, it, rr, ms = pcg.solve(b, rtol=1e-10, maxit=1000)
+    out["pcg_config2"] = {"workload": "PCG + IC0 on the config-2 matrix (7-pt 64^3, diag 6.01), "
+                                      "rtol 1e-10, b = gen_vector(n, 7)",
+                          "iterations": it, "relres": rr, "solve_ms": ms,
+                          "ms_per_iteration": ms / max(it, 1), "setup_s": setup}
+    pcg.close()
     return out
 
 

@@ -95,6 +95,9 @@ sfg_status sfg_plan_info(const sfg_plan* plan, int32_t* combo, int32_t* n,
 /* Replace the input vectors (st.vin = ...): nsys*n doubles, system-major,
  * host memory (pinned or pageable).  Asynchronous on the plan stream. */
 sfg_status sfg_set_vin(sfg_plan* plan, const double* vin_host);
+/* The same from device memory of the plan's device (zero-copy pipelines such
+ * as sfg_pcg_solve feed one plan's output to another's input). */
+sfg_status sfg_set_vin_device(sfg_plan* plan, const double* vin_device);
 /* Replace the matrix values, same sparsity (make_state on a matrix with the
  * pattern of the plan's, matrix.hpp:98-128): nsys*nnz(M) doubles in the
  * plan_create layout.  Re-derives every numeric operand on the device; the
@@ -192,6 +195,26 @@ sfg_status sfg_bench_executions(sfg_plan* plan, int32_t reps, int32_t unfused,
  * reciprocal path. */
 sfg_status sfg_selftest_division(int64_t n, uint64_t seed, int64_t* mismatches,
                                  int64_t* fast_path);
+
+/* Preconditioned conjugate gradients (the iterative solver that
+ * repeats the executor) ------------------------------------------------------
+ * A: SPD, CSC.  Setup factors A with IC0 (a combo-5 plan, bit-exact with the
+ * reference's ic0_column) and builds a combo-8 plan on the factor, whose fused
+ * forward/backward solve applies M^-1 = L^-T L^-1 each iteration.  The
+ * vector algebra (SpMV, dots with deterministic two-pass reductions, axpys)
+ * runs on the device; the host reads the residual every `check` iterations.
+ * Returns SFG_ERR_FACTORIZATION if IC0 breaks down (sfg_pcg_plans gives the
+ * factor plan for sfg_last_error). */
+typedef struct sfg_pcg sfg_pcg;
+sfg_status sfg_pcg_create(int32_t n, const int32_t* colptr, const int32_t* rowidx,
+                          const double* values, sfg_pcg** out);
+/* x = A^-1 b to ||b - A x|| <= rtol ||b|| (recursive residual) or maxit
+ * iterations; iters / relres / ms (device time) are optional outputs. */
+sfg_status sfg_pcg_solve(sfg_pcg* pcg, const double* b_host, double* x_host, double rtol,
+                         int32_t maxit, int32_t check, int32_t* iters, double* relres,
+                         float* ms);
+sfg_status sfg_pcg_plans(const sfg_pcg* pcg, sfg_plan** factor_plan, sfg_plan** solve_plan);
+sfg_status sfg_pcg_destroy(sfg_pcg* pcg);
 
 /* Fixtures (replaces fixtures.hpp generators + the BASELINE configs) -------
  * Generated matrices are returned through an opaque handle. */

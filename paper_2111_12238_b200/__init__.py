@@ -8,7 +8,7 @@ fallback.
 """
 from .api import (COMBOS, CscMatrix, DepDag, FactorizationError, FusedPartitioning,
                   FusedSchedule, InterDep, InvalidMatrixError, KernelState, LevelInfo,
-                  NoDeviceError, ParseError, build_g1, build_g2, collect_outputs,
+                  NoDeviceError, PCG, ParseError, build_g1, build_g2, collect_outputs,
                   compute_reuse, config5_systems, config_matrix, execute_fused,
                   execute_unfused, gen_banded_spd, gen_grid_laplacian,
                   gen_vector, inter_dag, joint_dag, level_info,
@@ -18,7 +18,7 @@ from .api import (COMBOS, CscMatrix, DepDag, FactorizationError, FusedPartitioni
 __all__ = [
     "COMBOS", "CscMatrix", "DepDag", "FactorizationError", "FusedPartitioning",
     "FusedSchedule", "InterDep", "InvalidMatrixError", "KernelState", "LevelInfo",
-    "NoDeviceError", "ParseError", "build_g1", "build_g2", "collect_outputs",
+    "NoDeviceError", "PCG", "ParseError", "build_g1", "build_g2", "collect_outputs",
     "compute_reuse", "config5_systems", "config_matrix", "execute_fused",
     "execute_unfused", "gen_banded_spd", "gen_grid_laplacian", "gen_vector",
     "inter_dag", "joint_dag", "level_info", "make_fused_schedule",

@@ -437,6 +437,53 @@ def gen_vector(n: int, seed: int) -> np.ndarray:
     return out[:n]
 
 
+class PCG:
+    """Preconditioned CG on the GPU with the IC0 factor (combo 5) and the fused
+    forward/backward solve (combo 8) as M^-1 (sfg_pcg_*)."""
+
+    def __init__(self, M: CscMatrix):
+        self.L = abi.load()
+        self.n = M.n
+        cp = np.ascontiguousarray(M.colptr, np.int32)
+        ri = np.ascontiguousarray(M.rowidx, np.int32)
+        va = np.ascontiguousarray(M.values, np.float64)
+        h = C.c_void_p()
+        st = self.L.sfg_pcg_create(M.n, ptr(cp, i32p), ptr(ri, i32p), ptr(va, f64p), C.byref(h))
+        self.h = h.value
+        if st != abi.SFG_OK:
+            fac = C.c_void_p()
+            if self.h:
+                self.L.sfg_pcg_plans(self.h, C.byref(fac), None)
+            try:
+                _raise(self.L, fac.value, st, "pcg setup")
+            finally:
+                self.close()
+
+    def solve(self, b: np.ndarray, rtol: float = 1e-10, maxit: int = 1000, check: int = 1):
+        """Returns (x, iterations, relative residual, device ms)."""
+        bb = np.ascontiguousarray(b, np.float64)
+        x = np.empty(self.n, np.float64)
+        it = C.c_int32()
+        rr = C.c_double()
+        ms = C.c_float()
+        st = self.L.sfg_pcg_solve(self.h, ptr(bb, f64p), ptr(x, f64p), rtol, maxit, check,
+                                  C.byref(it), C.byref(rr), C.byref(ms))
+        if st != abi.SFG_OK:
+            raise RuntimeError(f"pcg solve failed with status {st}")
+        return x, it.value, rr.value, ms.value
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.L.sfg_pcg_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 class ParseError(RuntimeError):
     """types.hpp:33-36 (Matrix Market and permutation files)."""
 

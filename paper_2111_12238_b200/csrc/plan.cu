@@ -1468,8 +1468,9 @@ sfg_status sfg_plan_info(const sfg_plan* P, int32_t* combo, int32_t* n, int32_t*
   return SFG_OK;
 }
 
-sfg_status sfg_set_vin(sfg_plan* P, const double* vin_host) {
-  if (!P || !vin_host || P->combo == 7 || P->combo == 3)
+namespace {
+sfg_status set_vin_impl(sfg_plan* P, const double* src, cudaMemcpyKind kind) {
+  if (!P || !src || P->combo == 7 || P->combo == 3)
     return SFG_ERR_INVALID_ARGUMENT;
   return guarded(P, [&] {
     DeviceScope ds(P->device);
@@ -1478,15 +1479,22 @@ sfg_status sfg_set_vin(sfg_plan* P, const double* vin_host) {
     if (nv == 0)
       return SFG_OK;
     if (P->nsys == 1) {
-      SFG_CUDA(cudaMemcpyAsync(P->vin.p, vin_host, sizeof(double) * (size_t)nv,
-                               cudaMemcpyHostToDevice, P->stream));
+      SFG_CUDA(cudaMemcpyAsync(P->vin.p, src, sizeof(double) * (size_t)nv, kind, P->stream));
     } else {
-      SFG_CUDA(cudaMemcpyAsync(P->staging.p, vin_host, sizeof(double) * (size_t)nv,
-                               cudaMemcpyHostToDevice, P->stream));
+      SFG_CUDA(cudaMemcpyAsync(P->staging.p, src, sizeof(double) * (size_t)nv, kind, P->stream));
       interleave(P->staging.p, P->n, P->nsys, P->vin.p, P->stream);
     }
     return SFG_OK;
   });
+}
+} // namespace
+
+sfg_status sfg_set_vin(sfg_plan* P, const double* vin_host) {
+  return set_vin_impl(P, vin_host, cudaMemcpyHostToDevice);
+}
+
+sfg_status sfg_set_vin_device(sfg_plan* P, const double* vin_device) {
+  return set_vin_impl(P, vin_device, cudaMemcpyDeviceToDevice);
 }
 
 namespace {
