@@ -1,0 +1,8 @@
+mkdir -p gpurun_out
+timeout 600 python -m pytest tests/test_gpu_parity.py -m gpu -x -q -p no:cacheprovider -k "golden_outputs or config_full or breakdown or pcg or set_values" > gpurun_out/exp22.txt 2>&1; echo rc=$? >> gpurun_out/exp22.txt
+run() {
+  envs="$1"; shift
+  timeout 300 env $envs python bench.py --steps 10 --warmup 3 --no-cpu-baseline --no-extras "$@" > /tmp/o.json 2>/tmp/e.txt
+  python -c "import json,sys;d=json.load(open('/tmp/o.json'));print('$envs $* ms=%.3f kernel=%.3f unfused=%.3f'%(d['ms_per_step'],d['roofline']['kernel_ms'],d['unfused']['ms_per_step']))" >> gpurun_out/exp22.txt 2>&1 || (echo "$envs $* FAILED" >> gpurun_out/exp22.txt; tail -3 /tmp/e.txt >> gpurun_out/exp22.txt)
+}
+for c in 2 3 4; do run "SFG_X=0" --config $c; done
