@@ -116,6 +116,40 @@ __global__ void codes_kernel(const int32_t* __restrict__ ptr, const int32_t* __r
   atomicMax(width, wmax);
 }
 
+// One thread per position: its step-stream record (S == 1).
+__global__ void stream_fill_kernel(const int32_t* __restrict__ ptr, const double* __restrict__ val,
+                                   int32_t n, int dir, const int32_t* __restrict__ cstart,
+                                   const int32_t* __restrict__ chain_of,
+                                   const int32_t* __restrict__ cskew,
+                                   const int32_t* __restrict__ code,
+                                   const int64_t* __restrict__ sofs, int32_t* __restrict__ srow,
+                                   int32_t* __restrict__ scode, double* __restrict__ sval,
+                                   int* too_wide) {
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n;
+       p += (int64_t)gridDim.x * blockDim.x) {
+    const int c = chain_of[p];
+    const int g = c >> 5, b = c & 31;
+    const int o = (int)p - cstart[c];
+    const int64_t rec = sofs[g] + (int64_t)(cskew[c] + o) * 32 + b;
+    const int r = dir > 0 ? (int)p : n - 1 - (int)p;
+    const int e0 = ptr[r], e1 = ptr[r + 1];
+    const bool chained = o > 0;
+    const int nd = e1 - e0 - 1 - (chained ? 1 : 0);
+    if (nd > kStreamChn) {
+      atomicOr(too_wide, 1);
+      continue;
+    }
+    srow[rec] = r;
+#pragma unroll
+    for (int a = 0; a < kStreamChn; ++a) {
+      scode[rec * kStreamChn + a] = a < nd ? code[e0 + a] : n; // padding: the zero row
+      sval[rec * (kStreamChn + 2) + a] = a < nd ? val[e0 + a] : 0.0;
+    }
+    sval[rec * (kStreamChn + 2) + kStreamChn] = chained ? val[e1 - 2] : 0.0;
+    sval[rec * (kStreamChn + 2) + kStreamChn + 1] = val[e1 - 1];
+  }
+}
+
 // ---------------------------------------------------------------------------
 // executor
 // ---------------------------------------------------------------------------
@@ -138,6 +172,10 @@ __device__ __forceinline__ void cp8(void* dst, const void* src) {
   // cp.async.wait_group (which has one), so the compiler may interleave the
   // stages' independent shared-memory loads with the copy issue
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(src));
+}
+__device__ __forceinline__ void cp16(void* dst, const void* src) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src));
 }
 __device__ __forceinline__ void cp4(void* dst, const void* src) {
   const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
@@ -448,6 +486,174 @@ __global__ void __launch_bounds__(kMThreads) k_mline(const MLineArgs A) {
   }
 }
 
+// Single-system multi-chain executor on the step stream: lane b owns chain
+// b of the group; per step it copies its own record (4 dependency codes, 6
+// values, row) with three coalesced 16-byte copies four steps ahead, gathers
+// the right-hand side and the external dependency words two steps ahead, and
+// completes its row from shared memory (ring for in-group dependencies).
+constexpr int kQ1 = 5; // record slots: steps i .. i+4
+constexpr int kX1 = 3; // gathered-word slots: steps i .. i+2
+struct alignas(16) Ml1Warp {
+  double v[kQ1][32][kStreamChn + 2];
+  int32_t cd[kQ1][32][kStreamChn];
+  int32_t row[kQ1][32];
+  unsigned long long x[kX1][32][kStreamChn];
+  unsigned long long rhs[kX1][32];
+  double ring[kRing][32];
+};
+
+__global__ void __launch_bounds__(kMThreads) k_mline1(const MLineArgs A) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Ml1Warp& W = reinterpret_cast<Ml1Warp*>(smem_raw)[threadIdx.x >> 5];
+  const int lane = threadIdx.x & 31;
+  const int total = A.seg_end - A.seg_begin;
+  for (;;) {
+    unsigned long long w0 = 0;
+    if (lane == 0)
+      w0 = atomicAdd(A.counter, 1ull);
+    const long long wi = (long long)__shfl_sync(FULL, w0, 0);
+    if (wi >= total)
+      break;
+    const int item = A.seg_begin + (int)wi;
+    const bool spmv4 = A.combo == 4 && item >= A.f_ngroup;
+    const bool spmv2 = A.combo == 2 && item < A.f_ngroup;
+    if (spmv4 || spmv2) { // SpMV row blocks (see k_mline)
+      const int blk = spmv4 ? item - A.f_ngroup : item;
+      const double* xsrc = spmv4 ? A.vmid : A.vin;
+      const int r = blk * 32 + lane;
+      if (spmv4) {
+        const int rl = min(blk * 32 + 31, A.n - 1);
+        if (lane == 0) {
+          const int pl = __ldg(A.ar_ptr + rl + 1) - 1;
+          if (pl >= 0) {
+            const int jl = __ldg(A.ar_idx + pl);
+            while (is_sent_hi(ld_relaxed_u64(A.vmid + jl)))
+              __nanosleep(1000);
+          }
+        }
+        __syncwarp();
+      }
+      if (r < A.n) {
+        double acc = 0.0;
+        for (int p = __ldg(A.ar_ptr + r); p < __ldg(A.ar_ptr + r + 1); ++p) {
+          const int j = __ldg(A.ar_idx + p);
+          unsigned long long w = ld_relaxed_u64(xsrc + j);
+          while (is_sent_hi(w)) {
+            __nanosleep(1000);
+            w = ld_relaxed_u64(xsrc + j);
+          }
+          acc = __dadd_rn(acc, __dmul_rn(__ldg(A.ar_val + p), __longlong_as_double((long long)w)));
+        }
+        if (spmv4)
+          A.vout[r] = acc;
+        else
+          publish_f64(A.vmid + r, acc);
+      }
+      continue;
+    }
+    const bool second = item >= A.f_ngroup;
+    const bool bwd = second && A.combo == 8;
+    const int g = second ? __ldg((bwd ? A.b_gorder : A.f_gorder) + (item - A.f_ngroup))
+                         : __ldg(A.f_gorder + item);
+    const int T = __ldg((bwd ? A.b_gsteps : A.f_gsteps) + g);
+    const int64_t base = __ldg((bwd ? A.b_sofs : A.f_sofs) + g) + lane;
+    const int32_t* srow = bwd ? A.b_srow : A.f_srow;
+    const int32_t* scode = bwd ? A.b_scode : A.f_scode;
+    const double* sval = bwd ? A.b_sval : A.f_sval;
+    double* xo = second ? A.vout : A.vmid;
+    const double* rhs_vec = second ? A.vmid : A.vin;
+    const int kern = second ? 2 : 1;
+    double carry = 0.0;
+    bool started = false;
+    __syncwarp();
+#pragma unroll 1
+    for (int i = -4; i < T; ++i) {
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+      __syncwarp();
+      // ---- record of step i+4
+      if (i + 4 < T) {
+        const int q = (i + 4) % kQ1;
+        const int64_t rec = base + (int64_t)(i + 4) * 32;
+        const double* vr = sval + rec * (kStreamChn + 2);
+        cp16(&W.v[q][lane][0], vr);
+        cp16(&W.v[q][lane][2], vr + 2);
+        cp16(&W.v[q][lane][4], vr + 4);
+        cp16(&W.cd[q][lane][0], scode + rec * kStreamChn);
+        cp4(&W.row[q][lane], srow + rec);
+      }
+      // ---- right-hand side and external words of step i+2
+      if (i + 2 >= 0 && i + 2 < T) {
+        const int q = (i + 2) % kQ1, qx = (i + 2) % kX1;
+        const int r = W.row[q][lane];
+        if (r >= 0) {
+          cp8(&W.rhs[qx][lane], rhs_vec + r);
+#pragma unroll
+          for (int a = 0; a < kStreamChn; ++a) {
+            const int cd = W.cd[q][lane][a];
+            if (cd >= 0)
+              cp8(&W.x[qx][lane][a], xo + cd);
+          }
+        }
+      }
+      asm volatile("cp.async.commit_group;" ::: "memory");
+      // ---- row of step i
+      if (i >= 0) {
+        const int q = i % kQ1, qx = i % kX1;
+        const int r = W.row[q][lane];
+        if (r >= 0) {
+          const double d = W.v[q][lane][kStreamChn + 1];
+          const double rd = __drcp_rn(d);
+          unsigned long long rw = W.rhs[qx][lane];
+          int cds[kStreamChn];
+          unsigned long long wd[kStreamChn];
+#pragma unroll
+          for (int a = 0; a < kStreamChn; ++a) {
+            const int cd = W.cd[q][lane][a];
+            cds[a] = cd;
+            if (cd >= 0) {
+              wd[a] = W.x[qx][lane][a];
+            } else {
+              const int t = -1 - cd;
+              wd[a] = (unsigned long long)__double_as_longlong(
+                  W.ring[(i - (t >> 5)) & (kRing - 1)][t & 31]);
+            }
+          }
+          for (;;) {
+            bool pending = is_sent_hi(rw);
+#pragma unroll
+            for (int a = 0; a < kStreamChn; ++a)
+              pending |= is_sent_hi(wd[a]);
+            if (!pending)
+              break;
+            if (is_sent_hi(rw))
+              rw = ld_relaxed_u64(rhs_vec + r);
+#pragma unroll
+            for (int a = 0; a < kStreamChn; ++a)
+              if (is_sent_hi(wd[a]))
+                wd[a] = ld_relaxed_u64(xo + cds[a]);
+          }
+          double acc = __longlong_as_double((long long)rw);
+#pragma unroll
+          for (int a = 0; a < kStreamChn; ++a)
+            acc = __dsub_rn(acc, __dmul_rn(W.v[q][lane][a], __longlong_as_double((long long)wd[a])));
+          if (started)
+            acc = __dsub_rn(acc, __dmul_rn(W.v[q][lane][kStreamChn], carry));
+          if (d == 0.0)
+            report_error(A.err, kern, bwd ? A.n - 1 - r : r, r);
+          const double xv = div_with_rcp(acc, d, rd);
+          publish_f64(xo + r, xv);
+          W.ring[i & (kRing - 1)][lane] = xv;
+          carry = xv;
+          started = true;
+        }
+      }
+      __syncwarp();
+    }
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    __syncwarp();
+  }
+}
+
 template <int S, int CHN, int DX> void launch_scd(const MLineArgs& a, cudaStream_t s) {
   // single-system plans are latency-bound: one CTA per SM keeps the solve
   // warps from sharing schedulers with waiting warps (measured on C1)
@@ -507,13 +713,14 @@ void build_mline(const int32_t* ptr, const int32_t* idx, int32_t n, int dir, int
   build_chains(ptr, idx, n, dir, 1, 1, max_len, ch, s);
   out.nchain = ch.nchain;
   out.cstart = std::move(ch.cstart);
+  out.chain_of = std::move(ch.chain_of);
   const int32_t nc = out.nchain;
   out.ngroup = (nc + B - 1) / B;
   const int32_t ng = out.ngroup;
   out.cskew.alloc(nc);
   out.gsteps.alloc(ng);
   SFG_CUDA(cudaMemsetAsync(out.cskew.p, 0, sizeof(int32_t) * (size_t)nc, s));
-  group_skew_kernel<<<mgrid(ng, 64), 64, 0, s>>>(ptr, idx, n, dir, out.cstart.p, ch.chain_of.p, nc,
+  group_skew_kernel<<<mgrid(ng, 64), 64, 0, s>>>(ptr, idx, n, dir, out.cstart.p, out.chain_of.p, nc,
                                                   B, ng, out.cskew.p, out.gsteps.p);
   count_launch();
   SFG_CUDA(cudaGetLastError());
@@ -524,7 +731,7 @@ void build_mline(const int32_t* ptr, const int32_t* idx, int32_t n, int dir, int
   DBuf<uint64_t> keys(nnz > 0 ? nnz : 1);
   DBuf<int> width(1);
   SFG_CUDA(cudaMemsetAsync(width.p, 0, sizeof(int), s));
-  codes_kernel<<<mgrid(n), 256, 0, s>>>(ptr, idx, n, dir, out.cstart.p, ch.chain_of.p,
+  codes_kernel<<<mgrid(n), 256, 0, s>>>(ptr, idx, n, dir, out.cstart.p, out.chain_of.p,
                                          out.cskew.p, B, out.code.p, keys.p, width.p);
   count_launch();
   SFG_CUDA(cudaGetLastError());
@@ -548,9 +755,63 @@ void build_mline(const int32_t* ptr, const int32_t* idx, int32_t n, int dir, int
     out.max_steps = v > out.max_steps ? v : out.max_steps;
 }
 
+void build_mline_stream(const int32_t* ptr, const double* val, int32_t n, int dir,
+                        MLineLayout& L, cudaStream_t s) {
+  L.stream = false;
+  if (L.S != 1 || L.ngroup == 0)
+    return;
+  std::vector<int32_t> gs((size_t)L.ngroup);
+  SFG_CUDA(cudaMemcpyAsync(gs.data(), L.gsteps.p, sizeof(int32_t) * gs.size(),
+                           cudaMemcpyDeviceToHost, s));
+  SFG_CUDA(cudaStreamSynchronize(s));
+  std::vector<int64_t> so((size_t)L.ngroup + 1, 0);
+  for (int32_t g = 0; g < L.ngroup; ++g)
+    so[(size_t)g + 1] = so[(size_t)g] + (int64_t)gs[(size_t)g] * 32;
+  L.nrec = so[(size_t)L.ngroup];
+  L.sofs.alloc((int64_t)L.ngroup + 1);
+  SFG_CUDA(cudaMemcpyAsync(L.sofs.p, so.data(), sizeof(int64_t) * so.size(),
+                           cudaMemcpyHostToDevice, s));
+  L.srow.alloc(L.nrec > 0 ? L.nrec : 1);
+  L.scode.alloc((L.nrec > 0 ? L.nrec : 1) * kStreamChn);
+  L.sval.alloc((L.nrec > 0 ? L.nrec : 1) * (kStreamChn + 2));
+  SFG_CUDA(cudaMemsetAsync(L.srow.p, 0xFF, sizeof(int32_t) * (size_t)std::max<int64_t>(L.nrec, 1), s));
+  DBuf<int> wide(1);
+  SFG_CUDA(cudaMemsetAsync(wide.p, 0, sizeof(int), s));
+  stream_fill_kernel<<<mgrid(n), 256, 0, s>>>(ptr, val, n, dir, L.cstart.p, L.chain_of.p, L.cskew.p,
+                                               L.code.p, L.sofs.p, L.srow.p, L.scode.p, L.sval.p,
+                                               wide.p);
+  count_launch();
+  SFG_CUDA(cudaGetLastError());
+  int hw = 0;
+  SFG_CUDA(cudaMemcpyAsync(&hw, wide.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+  SFG_CUDA(cudaStreamSynchronize(s));
+  L.stream = hw == 0;
+  if (!L.stream) {
+    L.srow.release();
+    L.scode.release();
+    L.sval.release();
+  }
+}
+
 void launch_mline(const MLineArgs& a, cudaStream_t s) {
   if (a.seg_end <= a.seg_begin)
     return;
+  if (a.S == 1 && a.use_stream) {
+    const size_t smem = (size_t)(kMThreads / 32) * sizeof(Ml1Warp);
+    SFG_CUDA(cudaFuncSetAttribute(k_mline1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int per_sm = 0;
+    SFG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_mline1, kMThreads, smem));
+    per_sm = a.blocks_per_sm > 0 ? std::min(std::max(per_sm, 1), a.blocks_per_sm) : 1;
+    const int64_t items = a.seg_end - a.seg_begin;
+    int64_t grid = (items + (kMThreads / 32) - 1) / (kMThreads / 32);
+    grid = std::min<int64_t>(grid, (int64_t)per_sm * sm_count());
+    if (grid >= 1) {
+      k_mline1<<<(unsigned)grid, kMThreads, smem, s>>>(a);
+      count_launch();
+      SFG_CUDA(cudaGetLastError());
+    }
+    return;
+  }
   switch (a.S) {
   case 1:
     launch_s<1>(a, s);

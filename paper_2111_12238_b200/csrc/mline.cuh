@@ -40,7 +40,26 @@ struct MLineLayout {
   DBuf<int32_t> glevel; // group -> group-DAG level (1-based)
   DBuf<int32_t> code;   // per CSR entry: >= 0 external row index, < 0 ring
                         // code -1 - (delta * 32 + b') (delta < kRing)
+  DBuf<int32_t> chain_of; // position -> chain
+  // Single-system step stream (S == 1, rows with <= kStreamChn dependencies):
+  // group g's records start at sofs[g]; record sofs[g] + step * 32 + lane is
+  // the row that lane computes at that step (srow, -1 = idle), its dependency
+  // codes scode[rec][kStreamChn] (padding: external row n, the zero row) and
+  // values sval[rec][kStreamChn + 2] (dependencies, carry coefficient,
+  // diagonal), so a warp fetches a whole step with a few coalesced copies.
+  bool stream = false;
+  int64_t nrec = 0;
+  DBuf<int64_t> sofs;
+  DBuf<int32_t> srow, scode;
+  DBuf<double> sval;
 };
+
+constexpr int32_t kStreamChn = 4;
+
+// (Re)builds the step stream from the current values (S == 1 only; sets
+// L.stream = false when a row has more than kStreamChn dependencies).
+void build_mline_stream(const int32_t* ptr, const double* val, int32_t n, int dir,
+                        MLineLayout& L, cudaStream_t s);
 
 // ptr/idx: CSR whose rows hold the dependencies in reference summation order
 // followed by the diagonal; position p is row p (dir = +1) or row n-1-p
@@ -79,6 +98,11 @@ struct MLineArgs {
   unsigned sleep_ns = 0; // back-off between re-polls of unpublished words
   int lookahead = 4;     // pipeline distance of the x gathers (2 or 4 steps)
   int32_t chn = 12; // staging width the kernel is instantiated for
+  // step streams (k_mline1, S == 1): forward / second-segment layouts
+  const int64_t *f_sofs = nullptr, *b_sofs = nullptr;
+  const int32_t *f_srow = nullptr, *f_scode = nullptr, *b_srow = nullptr, *b_scode = nullptr;
+  const double *f_sval = nullptr, *b_sval = nullptr;
+  bool use_stream = false;
   // diagnostics (SFG_TRACE): per work item {claim ns, first step ns, end ns,
   // stall cycles in cp.async waits << 32 | cycles in re-polls}
   unsigned long long* trace = nullptr;

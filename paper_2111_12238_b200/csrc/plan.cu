@@ -690,6 +690,12 @@ void do_inspect(sfg_plan* P) {
     if (combo == 8)
       build_mline(P->lt_ptr.p, P->lt_idx.p, n, -1, P->nsys, max_len, P->ml_b, s);
     P->use_mline = true;
+    const char* se = getenv("SFG_MLINE_STREAM");
+    if (P->nsys == 1 && !(se && std::string(se) == "0")) { // step streams (k_mline1)
+      build_mline_stream(P->lr_ptr.p, P->lr_val.p, n, +1, P->ml_f, s);
+      if (combo == 8)
+        build_mline_stream(P->lt_ptr.p, P->lt_val.p, n, -1, P->ml_b, s);
+    }
     if (getenv("SFG_MLINE_STATS")) {
       for (const MLineLayout* L : {&P->ml_f, &P->ml_b})
         if (L->nchain > 0)
@@ -831,6 +837,15 @@ MLineArgs mline_args(sfg_plan* P) {
   a.vout = P->vout.p;
   a.chn = std::max(P->ml_f.CHN, L2.CHN);
   a.trace = P->trace.p;
+  a.use_stream = P->ml_f.stream && L2.stream;
+  a.f_sofs = P->ml_f.sofs.p;
+  a.f_srow = P->ml_f.srow.p;
+  a.f_scode = P->ml_f.scode.p;
+  a.f_sval = P->ml_f.sval.p;
+  a.b_sofs = L2.sofs.p;
+  a.b_srow = L2.srow.p;
+  a.b_scode = L2.scode.p;
+  a.b_sval = L2.sval.p;
   if (const char* e = getenv("SFG_SLEEP_CAP"))
     a.sleep_ns = (unsigned)atoi(e);
   if (const char* e = getenv("SFG_MLINE_DX"))
@@ -1568,6 +1583,11 @@ sfg_status sfg_set_values(sfg_plan* P, const double* values_host) {
     }
     if (c == 7)
       dscal_vector(P->lc_ptr.p, P->lc_val.p, n, P->dvec.p, s);
+    if (P->use_mline && P->ml_f.stream) { // the step streams hold copies of the values
+      build_mline_stream(P->lr_ptr.p, P->lr_val.p, n, +1, P->ml_f, s);
+      if (c == 8)
+        build_mline_stream(P->lt_ptr.p, P->lt_val.p, n, -1, P->ml_b, s);
+    }
     if (P->use_ell || P->use_ws) { // the chain-ELL records hold copies of the values
       build_ell(P->lr_ptr.p, P->lr_idx.p, P->lr_val.p, n, S, +1, P->ell_chn, P->ch_f, P->ell_f, s);
       build_ell(P->lt_ptr.p, P->lt_idx.p, P->lt_val.p, n, S, -1, P->ell_chn, P->ch_b, P->ell_b, s);

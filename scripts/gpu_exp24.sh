@@ -1,0 +1,10 @@
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests -m gpu -x -q -p no:cacheprovider > gpurun_out/exp24.txt 2>&1; echo rc=$? >> gpurun_out/exp24.txt
+run() {
+  envs="$1"; shift
+  timeout 300 env $envs python bench.py --steps 10 --warmup 3 --no-cpu-baseline --no-extras "$@" > /tmp/o.json 2>/tmp/e.txt
+  python -c "import json,sys;d=json.load(open('/tmp/o.json'));print('$envs $* ms=%.3f kernel=%.3f unfused=%.3f'%(d['ms_per_step'],d['roofline']['kernel_ms'],d['unfused']['ms_per_step']))" >> gpurun_out/exp24.txt 2>&1 || (echo "$envs $* FAILED" >> gpurun_out/exp24.txt; tail -3 /tmp/e.txt >> gpurun_out/exp24.txt)
+}
+run "SFG_X=0" --config 1
+run "SFG_MLINE_STREAM=0" --config 1
+run "SFG_BLOCKS_PER_SM=2" --config 1
