@@ -124,7 +124,7 @@ __global__ void stream_fill_kernel(const int32_t* __restrict__ ptr, const double
                                    const int32_t* __restrict__ code,
                                    const int64_t* __restrict__ sofs, int32_t* __restrict__ srow,
                                    int32_t* __restrict__ scode, double* __restrict__ sval,
-                                   int* too_wide) {
+                                   int ch, int* too_wide) {
   for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n;
        p += (int64_t)gridDim.x * blockDim.x) {
     const int c = chain_of[p];
@@ -135,18 +135,17 @@ __global__ void stream_fill_kernel(const int32_t* __restrict__ ptr, const double
     const int e0 = ptr[r], e1 = ptr[r + 1];
     const bool chained = o > 0;
     const int nd = e1 - e0 - 1 - (chained ? 1 : 0);
-    if (nd > kStreamChn) {
+    if (nd > ch) {
       atomicOr(too_wide, 1);
       continue;
     }
     srow[rec] = r;
-#pragma unroll
-    for (int a = 0; a < kStreamChn; ++a) {
-      scode[rec * kStreamChn + a] = a < nd ? code[e0 + a] : n; // padding: the zero row
-      sval[rec * (kStreamChn + 2) + a] = a < nd ? val[e0 + a] : 0.0;
+    for (int a = 0; a < ch; ++a) {
+      scode[rec * ch + a] = a < nd ? code[e0 + a] : n; // padding: the zero row
+      sval[rec * (ch + 2) + a] = a < nd ? val[e0 + a] : 0.0;
     }
-    sval[rec * (kStreamChn + 2) + kStreamChn] = chained ? val[e1 - 2] : 0.0;
-    sval[rec * (kStreamChn + 2) + kStreamChn + 1] = val[e1 - 1];
+    sval[rec * (ch + 2) + ch] = chained ? val[e1 - 2] : 0.0;
+    sval[rec * (ch + 2) + ch + 1] = val[e1 - 1];
   }
 }
 
@@ -488,23 +487,27 @@ __global__ void __launch_bounds__(kMThreads) k_mline(const MLineArgs A) {
 
 // Single-system multi-chain executor on the step stream: lane b owns chain
 // b of the group; per step it copies its own record (4 dependency codes, 6
-// values, row) with three coalesced 16-byte copies four steps ahead, gathers
-// the right-hand side and the external dependency words two steps ahead, and
+// values, row) with coalesced 16-byte copies kRA1 steps ahead, gathers the
+// right-hand side and the external dependency words kXA1 steps ahead, and
 // completes its row from shared memory (ring for in-group dependencies).
-constexpr int kQ1 = 5; // record slots: steps i .. i+4
-constexpr int kX1 = 3; // gathered-word slots: steps i .. i+2
-struct alignas(16) Ml1Warp {
-  double v[kQ1][32][kStreamChn + 2];
-  int32_t cd[kQ1][32][kStreamChn];
+constexpr int kXA1 = 2;        // gathers run kXA1 steps ahead
+constexpr int kRA1 = 2 * kXA1; // records run kRA1 steps ahead
+constexpr int kQ1 = kRA1 + 1;  // record slots: steps i .. i+kRA1
+constexpr int kX1 = kXA1 + 1;  // gathered-word slots: steps i .. i+kXA1
+template <int CH> struct alignas(16) Ml1Warp {
+  double v[kQ1][32][CH + 2];
+  int32_t cd[kQ1][32][CH];
   int32_t row[kQ1][32];
-  unsigned long long x[kX1][32][kStreamChn];
+  unsigned long long x[kX1][32][CH];
   unsigned long long rhs[kX1][32];
   double ring[kRing][32];
 };
 
+template <int CH>
 __global__ void __launch_bounds__(kMThreads) k_mline1(const MLineArgs A) {
+  static_assert(CH == 2 || CH == 4, "record widths of 32 or 48 bytes");
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  Ml1Warp& W = reinterpret_cast<Ml1Warp*>(smem_raw)[threadIdx.x >> 5];
+  Ml1Warp<CH>& W = reinterpret_cast<Ml1Warp<CH>*>(smem_raw)[threadIdx.x >> 5];
   const int lane = threadIdx.x & 31;
   const int total = A.seg_end - A.seg_begin;
   for (;;) {
@@ -565,30 +568,40 @@ __global__ void __launch_bounds__(kMThreads) k_mline1(const MLineArgs A) {
     const int kern = second ? 2 : 1;
     double carry = 0.0;
     bool started = false;
+    unsigned long long tr_claim = 0, tr_first = 0, poll_cyc = 0, d_cyc = 0;
+    if (A.trace)
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tr_claim));
     __syncwarp();
 #pragma unroll 1
-    for (int i = -4; i < T; ++i) {
-      asm volatile("cp.async.wait_group 1;" ::: "memory");
+    for (int i = -kRA1; i < T; ++i) {
+      if (A.trace && i == 0)
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tr_first));
+      // commit groups <= i - kXA1 complete: records of steps <= i + kXA1,
+      // gathers of steps <= i
+      asm volatile("cp.async.wait_group %0;" ::"n"(kXA1 - 1) : "memory");
       __syncwarp();
-      // ---- record of step i+4
-      if (i + 4 < T) {
-        const int q = (i + 4) % kQ1;
-        const int64_t rec = base + (int64_t)(i + 4) * 32;
-        const double* vr = sval + rec * (kStreamChn + 2);
-        cp16(&W.v[q][lane][0], vr);
-        cp16(&W.v[q][lane][2], vr + 2);
-        cp16(&W.v[q][lane][4], vr + 4);
-        cp16(&W.cd[q][lane][0], scode + rec * kStreamChn);
+      // ---- record of step i+kRA1
+      if (i + kRA1 < T) {
+        const int q = (i + kRA1) % kQ1;
+        const int64_t rec = base + (int64_t)(i + kRA1) * 32;
+        const double* vr = sval + rec * (CH + 2);
+#pragma unroll
+        for (int h = 0; h < CH + 2; h += 2)
+          cp16(&W.v[q][lane][h], vr + h);
+        if (CH == 4)
+          cp16(&W.cd[q][lane][0], scode + rec * CH);
+        else
+          cp8(&W.cd[q][lane][0], scode + rec * CH);
         cp4(&W.row[q][lane], srow + rec);
       }
-      // ---- right-hand side and external words of step i+2
-      if (i + 2 >= 0 && i + 2 < T) {
-        const int q = (i + 2) % kQ1, qx = (i + 2) % kX1;
+      // ---- right-hand side and external words of step i+kXA1
+      if (i + kXA1 >= 0 && i + kXA1 < T) {
+        const int q = (i + kXA1) % kQ1, qx = (i + kXA1) % kX1;
         const int r = W.row[q][lane];
         if (r >= 0) {
           cp8(&W.rhs[qx][lane], rhs_vec + r);
 #pragma unroll
-          for (int a = 0; a < kStreamChn; ++a) {
+          for (int a = 0; a < CH; ++a) {
             const int cd = W.cd[q][lane][a];
             if (cd >= 0)
               cp8(&W.x[qx][lane][a], xo + cd);
@@ -597,17 +610,18 @@ __global__ void __launch_bounds__(kMThreads) k_mline1(const MLineArgs A) {
       }
       asm volatile("cp.async.commit_group;" ::: "memory");
       // ---- row of step i
+      const long long dc0 = A.trace ? clock64() : 0;
       if (i >= 0) {
         const int q = i % kQ1, qx = i % kX1;
         const int r = W.row[q][lane];
         if (r >= 0) {
-          const double d = W.v[q][lane][kStreamChn + 1];
+          const double d = W.v[q][lane][CH + 1];
           const double rd = __drcp_rn(d);
           unsigned long long rw = W.rhs[qx][lane];
-          int cds[kStreamChn];
-          unsigned long long wd[kStreamChn];
+          int cds[CH];
+          unsigned long long wd[CH];
 #pragma unroll
-          for (int a = 0; a < kStreamChn; ++a) {
+          for (int a = 0; a < CH; ++a) {
             const int cd = W.cd[q][lane][a];
             cds[a] = cd;
             if (cd >= 0) {
@@ -618,26 +632,29 @@ __global__ void __launch_bounds__(kMThreads) k_mline1(const MLineArgs A) {
                   W.ring[(i - (t >> 5)) & (kRing - 1)][t & 31]);
             }
           }
+          const long long pc0 = A.trace ? clock64() : 0;
           for (;;) {
             bool pending = is_sent_hi(rw);
 #pragma unroll
-            for (int a = 0; a < kStreamChn; ++a)
+            for (int a = 0; a < CH; ++a)
               pending |= is_sent_hi(wd[a]);
             if (!pending)
               break;
             if (is_sent_hi(rw))
               rw = ld_relaxed_u64(rhs_vec + r);
 #pragma unroll
-            for (int a = 0; a < kStreamChn; ++a)
+            for (int a = 0; a < CH; ++a)
               if (is_sent_hi(wd[a]))
                 wd[a] = ld_relaxed_u64(xo + cds[a]);
           }
+          if (A.trace)
+            poll_cyc += clock64() - pc0;
           double acc = __longlong_as_double((long long)rw);
 #pragma unroll
-          for (int a = 0; a < kStreamChn; ++a)
+          for (int a = 0; a < CH; ++a)
             acc = __dsub_rn(acc, __dmul_rn(W.v[q][lane][a], __longlong_as_double((long long)wd[a])));
           if (started)
-            acc = __dsub_rn(acc, __dmul_rn(W.v[q][lane][kStreamChn], carry));
+            acc = __dsub_rn(acc, __dmul_rn(W.v[q][lane][CH], carry));
           if (d == 0.0)
             report_error(A.err, kern, bwd ? A.n - 1 - r : r, r);
           const double xv = div_with_rcp(acc, d, rd);
@@ -648,9 +665,28 @@ __global__ void __launch_bounds__(kMThreads) k_mline1(const MLineArgs A) {
         }
       }
       __syncwarp();
+      if (A.trace)
+        d_cyc += clock64() - dc0;
     }
     asm volatile("cp.async.wait_group 0;" ::: "memory");
     __syncwarp();
+    if (A.trace) {
+      unsigned long long pm = poll_cyc;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const unsigned long long v = __shfl_xor_sync(FULL, pm, o);
+        pm = v > pm ? v : pm;
+      }
+      if (lane == 0) {
+        unsigned long long te;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(te));
+        unsigned long long* tr = A.trace + (size_t)item * 4;
+        tr[0] = tr_claim;
+        tr[1] = tr_first;
+        tr[2] = te;
+        tr[3] = (d_cyc << 32) | (pm & 0xffffffffull);
+      }
+    }
   }
 }
 
@@ -771,15 +807,16 @@ void build_mline_stream(const int32_t* ptr, const double* val, int32_t n, int di
   L.sofs.alloc((int64_t)L.ngroup + 1);
   SFG_CUDA(cudaMemcpyAsync(L.sofs.p, so.data(), sizeof(int64_t) * so.size(),
                            cudaMemcpyHostToDevice, s));
+  L.sch = L.CHN <= 2 ? 2 : kStreamChn;
   L.srow.alloc(L.nrec > 0 ? L.nrec : 1);
-  L.scode.alloc((L.nrec > 0 ? L.nrec : 1) * kStreamChn);
-  L.sval.alloc((L.nrec > 0 ? L.nrec : 1) * (kStreamChn + 2));
+  L.scode.alloc((L.nrec > 0 ? L.nrec : 1) * L.sch);
+  L.sval.alloc((L.nrec > 0 ? L.nrec : 1) * (L.sch + 2));
   SFG_CUDA(cudaMemsetAsync(L.srow.p, 0xFF, sizeof(int32_t) * (size_t)std::max<int64_t>(L.nrec, 1), s));
   DBuf<int> wide(1);
   SFG_CUDA(cudaMemsetAsync(wide.p, 0, sizeof(int), s));
   stream_fill_kernel<<<mgrid(n), 256, 0, s>>>(ptr, val, n, dir, L.cstart.p, L.chain_of.p, L.cskew.p,
                                                L.code.p, L.sofs.p, L.srow.p, L.scode.p, L.sval.p,
-                                               wide.p);
+                                               L.sch, wide.p);
   count_launch();
   SFG_CUDA(cudaGetLastError());
   int hw = 0;
@@ -797,16 +834,18 @@ void launch_mline(const MLineArgs& a, cudaStream_t s) {
   if (a.seg_end <= a.seg_begin)
     return;
   if (a.S == 1 && a.use_stream) {
-    const size_t smem = (size_t)(kMThreads / 32) * sizeof(Ml1Warp);
-    SFG_CUDA(cudaFuncSetAttribute(k_mline1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    auto kern = a.stream_ch <= 2 ? k_mline1<2> : k_mline1<4>;
+    const size_t smem = (size_t)(kMThreads / 32) *
+                        (a.stream_ch <= 2 ? sizeof(Ml1Warp<2>) : sizeof(Ml1Warp<4>));
+    SFG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int per_sm = 0;
-    SFG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_mline1, kMThreads, smem));
+    SFG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kMThreads, smem));
     per_sm = a.blocks_per_sm > 0 ? std::min(std::max(per_sm, 1), a.blocks_per_sm) : 1;
     const int64_t items = a.seg_end - a.seg_begin;
     int64_t grid = (items + (kMThreads / 32) - 1) / (kMThreads / 32);
     grid = std::min<int64_t>(grid, (int64_t)per_sm * sm_count());
     if (grid >= 1) {
-      k_mline1<<<(unsigned)grid, kMThreads, smem, s>>>(a);
+      kern<<<(unsigned)grid, kMThreads, smem, s>>>(a);
       count_launch();
       SFG_CUDA(cudaGetLastError());
     }

@@ -48,6 +48,7 @@ struct MLineLayout {
   // values sval[rec][kStreamChn + 2] (dependencies, carry coefficient,
   // diagonal), so a warp fetches a whole step with a few coalesced copies.
   bool stream = false;
+  int32_t sch = 4; // record width (2 or kStreamChn dependencies)
   int64_t nrec = 0;
   DBuf<int64_t> sofs;
   DBuf<int32_t> srow, scode;
@@ -103,6 +104,7 @@ struct MLineArgs {
   const int32_t *f_srow = nullptr, *f_scode = nullptr, *b_srow = nullptr, *b_scode = nullptr;
   const double *f_sval = nullptr, *b_sval = nullptr;
   bool use_stream = false;
+  int32_t stream_ch = 4;
   // diagnostics (SFG_TRACE): per work item {claim ns, first step ns, end ns,
   // stall cycles in cp.async waits << 32 | cycles in re-polls}
   unsigned long long* trace = nullptr;

@@ -837,7 +837,8 @@ MLineArgs mline_args(sfg_plan* P) {
   a.vout = P->vout.p;
   a.chn = std::max(P->ml_f.CHN, L2.CHN);
   a.trace = P->trace.p;
-  a.use_stream = P->ml_f.stream && L2.stream;
+  a.use_stream = P->ml_f.stream && L2.stream && P->ml_f.sch == L2.sch;
+  a.stream_ch = P->ml_f.sch;
   a.f_sofs = P->ml_f.sofs.p;
   a.f_srow = P->ml_f.srow.p;
   a.f_scode = P->ml_f.scode.p;

@@ -1,5 +1,5 @@
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests -m gpu -x -q -p no:cacheprovider > gpurun_out/exp24.txt 2>&1; echo rc=$? >> gpurun_out/exp24.txt
+timeout 900 python -m pytest tests/test_gpu_parity.py -m gpu -x -q -p no:cacheprovider -k "golden_outputs or config_full or batch or multisystem or partitioning" > gpurun_out/exp24.txt 2>&1; echo rc=$? >> gpurun_out/exp24.txt
 run() {
   envs="$1"; shift
   timeout 300 env $envs python bench.py --steps 10 --warmup 3 --no-cpu-baseline --no-extras "$@" > /tmp/o.json 2>/tmp/e.txt

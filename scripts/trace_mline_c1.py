@@ -20,4 +20,4 @@ d = raw[3:3 + items * 4].view(np.uint64).reshape(items, 4)
 t0 = d[:, 0].min()
 for i in range(items):
     c, f, e = (d[i, :3] - t0) / 1e3
-    print(f"item {i:3d}: claim {c:8.1f} first {f:8.1f} end {e:8.1f} dur {e - f:8.1f} wait_cyc {int(d[i,3] >> 32):9d} poll_cyc {int(d[i,3] & 0xffffffff):9d}")
+    print(f"item {i:3d}: claim {c:8.1f} first {f:8.1f} end {e:8.1f} dur {e - f:8.1f} hi_cyc {int(d[i,3] >> 32):9d} poll_cyc {int(d[i,3] & 0xffffffff):9d}")
