@@ -142,10 +142,12 @@ __global__ void stream_fill_kernel(const int32_t* __restrict__ ptr, const double
     srow[rec] = r;
     for (int a = 0; a < ch; ++a) {
       scode[rec * ch + a] = a < nd ? code[e0 + a] : n; // padding: the zero row
-      sval[rec * (ch + 2) + a] = a < nd ? val[e0 + a] : 0.0;
+      sval[rec * (ch + 4) + a] = a < nd ? val[e0 + a] : 0.0;
     }
-    sval[rec * (ch + 2) + ch] = chained ? val[e1 - 2] : 0.0;
-    sval[rec * (ch + 2) + ch + 1] = val[e1 - 1];
+    sval[rec * (ch + 4) + ch] = chained ? val[e1 - 2] : 0.0;
+    sval[rec * (ch + 4) + ch + 1] = val[e1 - 1];
+    sval[rec * (ch + 4) + ch + 2] = __drcp_rn(val[e1 - 1]); // reciprocal off the step's chain
+    sval[rec * (ch + 4) + ch + 3] = 0.0;
   }
 }
 
@@ -495,7 +497,7 @@ constexpr int kRA1 = 2 * kXA1; // records run kRA1 steps ahead
 constexpr int kQ1 = kRA1 + 1;  // record slots: steps i .. i+kRA1
 constexpr int kX1 = kXA1 + 1;  // gathered-word slots: steps i .. i+kXA1
 template <int CH> struct alignas(16) Ml1Warp {
-  double v[kQ1][32][CH + 2];
+  double v[kQ1][32][CH + 4]; // deps, carry coefficient, diagonal, its reciprocal, pad
   int32_t cd[kQ1][32][CH];
   int32_t row[kQ1][32];
   unsigned long long x[kX1][32][CH];
@@ -584,9 +586,9 @@ __global__ void __launch_bounds__(kMThreads) k_mline1(const MLineArgs A) {
       if (i + kRA1 < T) {
         const int q = (i + kRA1) % kQ1;
         const int64_t rec = base + (int64_t)(i + kRA1) * 32;
-        const double* vr = sval + rec * (CH + 2);
+        const double* vr = sval + rec * (CH + 4);
 #pragma unroll
-        for (int h = 0; h < CH + 2; h += 2)
+        for (int h = 0; h < CH + 4; h += 2)
           cp16(&W.v[q][lane][h], vr + h);
         if (CH == 4)
           cp16(&W.cd[q][lane][0], scode + rec * CH);
@@ -616,7 +618,7 @@ __global__ void __launch_bounds__(kMThreads) k_mline1(const MLineArgs A) {
         const int r = W.row[q][lane];
         if (r >= 0) {
           const double d = W.v[q][lane][CH + 1];
-          const double rd = __drcp_rn(d);
+          const double rd = W.v[q][lane][CH + 2];
           unsigned long long rw = W.rhs[qx][lane];
           int cds[CH];
           unsigned long long wd[CH];
@@ -810,7 +812,7 @@ void build_mline_stream(const int32_t* ptr, const double* val, int32_t n, int di
   L.sch = L.CHN <= 2 ? 2 : kStreamChn;
   L.srow.alloc(L.nrec > 0 ? L.nrec : 1);
   L.scode.alloc((L.nrec > 0 ? L.nrec : 1) * L.sch);
-  L.sval.alloc((L.nrec > 0 ? L.nrec : 1) * (L.sch + 2));
+  L.sval.alloc((L.nrec > 0 ? L.nrec : 1) * (L.sch + 4));
   SFG_CUDA(cudaMemsetAsync(L.srow.p, 0xFF, sizeof(int32_t) * (size_t)std::max<int64_t>(L.nrec, 1), s));
   DBuf<int> wide(1);
   SFG_CUDA(cudaMemsetAsync(wide.p, 0, sizeof(int), s));

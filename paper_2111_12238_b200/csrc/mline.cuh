@@ -44,9 +44,10 @@ struct MLineLayout {
   // Single-system step stream (S == 1, rows with <= kStreamChn dependencies):
   // group g's records start at sofs[g]; record sofs[g] + step * 32 + lane is
   // the row that lane computes at that step (srow, -1 = idle), its dependency
-  // codes scode[rec][kStreamChn] (padding: external row n, the zero row) and
-  // values sval[rec][kStreamChn + 2] (dependencies, carry coefficient,
-  // diagonal), so a warp fetches a whole step with a few coalesced copies.
+  // codes scode[rec][sch] (padding: external row n, the zero row) and
+  // values sval[rec][sch + 4] (dependencies, carry coefficient, diagonal,
+  // its reciprocal RN(1/d), padding), so a warp fetches a whole step with a
+  // few coalesced copies.
   bool stream = false;
   int32_t sch = 4; // record width (2 or kStreamChn dependencies)
   int64_t nrec = 0;
