@@ -1,0 +1,91 @@
+"""Edge cases through the C-ABI, every executor, bit-exact against the oracle:
+empty and 1x1 systems, diagonal-only matrices (no dependencies, every chain
+of length 1), dense blocks (rows far wider than any staging width, so the
+long-row paths run), a single long chain (bidiagonal), and isolated rows."""
+import numpy as np
+import pytest
+
+import paper_2111_12238_b200 as sf
+from oracle.oracle import Csc
+
+pytestmark = pytest.mark.gpu
+
+COMBOS = (1, 2, 3, 4, 5, 6, 7, 8)
+EXECUTORS = ("default", "levels", "chain", "mline")
+
+
+def csc(D):
+    D = np.asarray(D, np.float64)
+    n = D.shape[0]
+    cp, ri, va = [0], [], []
+    for j in range(n):
+        for i in range(n):
+            if D[i, j] != 0.0:
+                ri.append(i)
+                va.append(D[i, j])
+        cp.append(len(ri))
+    return Csc(n, np.array(cp, np.int32), np.array(ri, np.int32), np.array(va, np.float64))
+
+
+def spd(n, bw, seed):
+    rng = np.random.default_rng(seed)
+    D = np.zeros((n, n))
+    for i in range(n):
+        for j in range(max(0, i - bw), i):
+            v = -rng.uniform(0.1, 1.0)
+            D[i, j] = D[j, i] = v
+    D[np.arange(n), np.arange(n)] = np.abs(D).sum(1) + 1.0
+    return D
+
+
+CASES = {
+    "n1": np.array([[3.0]]),
+    "diag": np.diag(np.arange(1.0, 40.0)),
+    "bidiag": np.eye(300) * 4 - np.eye(300, k=-1) - np.eye(300, k=1),
+    "dense40": spd(40, 40, 1),
+    "wide_rows": spd(120, 60, 2),       # rows of ~60 entries: beyond every staging width
+    "blocks": np.kron(np.eye(7), spd(9, 9, 3)),  # independent dense blocks
+}
+
+
+@pytest.mark.parametrize("executor", EXECUTORS)
+@pytest.mark.parametrize("name", sorted(CASES))
+def test_edge_cases_all_combos(orc, monkeypatch, name, executor):
+    if executor != "default":
+        monkeypatch.setenv("SFG_EXECUTOR", executor)
+    Mo = csc(CASES[name])
+    M = sf.CscMatrix(Mo.n, Mo.colptr, Mo.rowidx, Mo.values)
+    for combo in COMBOS:
+        want = orc.run_sequential(combo, Mo, 7)
+        st = sf.make_state(combo, M, seed=7)
+        st.execute_fused()
+        assert np.array_equal(st.collect_outputs(), want), (name, executor, combo)
+        st.execute_unfused()
+        assert np.array_equal(st.collect_outputs(), want), (name, executor, combo, "unfused")
+
+
+def test_empty_system():
+    M = sf.CscMatrix(0, np.zeros(1, np.int32), np.zeros(0, np.int32), np.zeros(0))
+    for combo in COMBOS:
+        st = sf.make_state(combo, M)
+        st.execute_fused()
+        assert st.collect_outputs().size == 0
+        st.execute_unfused()
+
+
+@pytest.mark.parametrize("nsys", (2, 4, 16, 32))
+def test_batched_edge_cases(orc, nsys):
+    for name in ("bidiag", "dense40", "wide_rows"):
+        Mo = csc(CASES[name])
+        rng = np.random.default_rng(nsys)
+        vals = np.concatenate([Mo.values * (1 + 0.01 * s) for s in range(nsys)])
+        vin = rng.uniform(-1, 1, nsys * Mo.n)
+        M = sf.CscMatrix(Mo.n, Mo.colptr, Mo.rowidx, Mo.values)
+        for combo in (1, 8):
+            st = sf.make_state(combo, M, nsys=nsys, values=vals, vin=vin)
+            st.execute_fused()
+            got = st.collect_outputs().reshape(nsys, -1)
+            for s in (0, nsys - 1):
+                Ms = Csc(Mo.n, Mo.colptr, Mo.rowidx, vals[s * Mo.nnz:(s + 1) * Mo.nnz])
+                want = orc.run_sequential(combo, Ms, 7, vin=vin[s * Mo.n:(s + 1) * Mo.n])
+                assert np.array_equal(got[s], want), (name, combo, nsys, s)
