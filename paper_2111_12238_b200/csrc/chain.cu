@@ -608,6 +608,17 @@ __global__ void __launch_bounds__(kThreads, 2) k_chain_sm(const ChainArgs A) {
     double cd = 1.0, cvc = 0.0, crd = 1.0;
     unsigned long long crhs = 0;
     double carry = 0.0, carry2 = 0.0;
+    if (bwd && pass1 && (A.phase & 1) && A.bwd_gate) { // fused launch only
+      // a backward chain cannot start before the forward solve has reached
+      // its first right-hand side: one lane sleeps on that word instead of
+      // the whole warp polling L2 while the forward solve still runs
+      if (lane == 0) {
+        const unsigned long long* w = reinterpret_cast<const unsigned long long*>(
+            rhs_vec + (size_t)row_of(0) * S);
+        while (is_sent_hi(ld_relaxed_u64(w)))
+          __nanosleep(A.bwd_gate);
+      }
+    }
     __syncwarp();
 #pragma unroll 1
     for (int t = -3; t < ntiles; ++t) {

@@ -77,6 +77,7 @@ struct ChainArgs {
   double* vout = nullptr;
   int blocks_per_sm = 0;
   int tile_rows = 0; // single-system tile height override (0 = default)
+  unsigned bwd_gate = 500; // ns a backward chain's first lane sleeps per check (0 = off)
   // optional timeline trace: per (work item, tile) {claim, partial done,
   // carry done} in %globaltimer ns (diagnostics only; null in production)
   unsigned long long* trace = nullptr;

@@ -882,6 +882,8 @@ ChainArgs chain_args(sfg_plan* P) {
   a.tail_ptr = P->tail_ptr.p;
   a.tile_rows = P->tile_rows;
   a.tail_rows = P->tail_rows.p;
+  if (const char* e = getenv("SFG_BWD_GATE"))
+    a.bwd_gate = (unsigned)atoi(e);
   a.ar_ptr = P->ar_ptr.p;
   a.ar_idx = P->ar_idx.p;
   a.ar_val = P->ar_val.p;
