@@ -13,7 +13,10 @@ per step.  One "exec" = one fused kernel-pair execution on one system.
 
 Multi-GPU: the systems are independent, so each rank runs its own batch of
 8 (weak scaling, no data-path collective); torch.distributed is used only
-for the barrier and the max-over-ranks of the timings.
+for the barrier and the max-over-ranks of the timings.  ``--config 1
+--shard-spmv`` runs config 1 with the solve on rank 0 and the SpMV rows
+sharded over the ranks (one point-to-point x exchange + a y all-gather over
+NCCL; strong scaling).
 """
 from __future__ import annotations
 
@@ -369,6 +372,94 @@ def run_ours(args, D: Dist):
     return line
 
 
+# ---------------------------------------------------------------------------
+# config 1 split across ranks: rank 0 solves, x slices travel
+# point-to-point over NCCL, every rank computes its rows of y, all-gather
+# ---------------------------------------------------------------------------
+def run_sharded(args, D: Dist):
+    import torch
+    import paper_2111_12238_b200 as sf
+    from paper_2111_12238_b200 import abi, shard
+    abi.set_device(D.local)
+    torch.cuda.set_device(D.local)
+    M = sf.config_matrix(1, size=args.size)
+    n = M.n
+    vin = sf.gen_vector(n, 7)
+    st = sf.make_state(4, M, seed=7, vin=vin)
+    st.inspect()
+    stream = torch.cuda.Stream()
+    with torch.cuda.stream(stream):
+        st.set_stream(stream.cuda_stream)
+        solve, spmv = shard.plan_callbacks(st, n)
+        if D.rank != 0:
+            solve = None
+        rowptr, colidx = shard.csr_pattern(M.colptr, M.rowidx, n)
+        S = shard.ShardedSpmv(getattr(D, "td", None), D.rank, D.world, n, rowptr, colidx,
+                              torch.device("cuda", D.local), solve=solve, spmv=spmv)
+        for _ in range(args.warmup):
+            S.step()
+        stream.synchronize()
+        D.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        l0 = st.launch_count()
+        with ClockSampler(D.local) as clk:
+            e0.record(stream)
+            for _ in range(args.steps):
+                y = S.step()
+            e1.record(stream)
+            e1.synchronize()
+        launches = st.launch_count() - l0
+        D.barrier()
+        ms = D.max(e0.elapsed_time(e1) / args.steps)
+        y_dev = y.cpu().numpy()
+
+        # e2e: b from pinned host memory into the plan (rank 0), y back to host
+        pin_b = abi.PinnedArray(n)
+        pin_b.array[:] = vin
+        y_host = torch.empty(n, dtype=torch.float64, pin_memory=True)
+        D.barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            if D.rank == 0:
+                st.set_vin(pin_b.array)
+            y_host.copy_(S.step(), non_blocking=True)
+            stream.synchronize()
+        e2e_s = D.max((time.perf_counter() - t0) / args.steps)
+        pin_b.free()
+    st.set_stream(None)
+    # parity of the timed result: the single-GPU fused combo 4 on rank 0
+    parity = None
+    if D.rank == 0:
+        ref = sf.make_state(4, M, seed=7, vin=vin)
+        ref.execute_fused()
+        want = ref.collect_outputs()[n:2 * n]
+        parity = bool(np.array_equal(y_dev, want) and np.array_equal(y_host.numpy(), want))
+        ref.close()
+    nnzL = lower_nnz(M)
+    peak, peak_src = hbm_peak()
+    abytes = algorithmic_bytes(1, n, nnzL, M.nnz)
+    st.close()
+    return {
+        "metric": METRIC, "value": 1e3 / ms, "unit": UNIT, "n_gpus": D.world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": CONFIG_NAME[1] + ", SpMV rows sharded over ranks",
+                   "baseline_config": 1, "combo": 4, "n": n, "nnz_A": M.nnz,
+                   "shards": S.shards, "x_ranges": S.ranges,
+                   "halo_rows": shard.halo_rows(S.shards, S.ranges),
+                   "exchange_bytes_per_step": S.exchanged_bytes(),
+                   "l2": "not flushed (whole working set %.1f MB < L2)" % (abytes / 1e6),
+                   "parallelism": f"solve on rank 0, SpMV row-sharded over {D.world} ranks"},
+        "gpu_launches": launches, "parity_vs_fused": parity,
+        "roofline": {"bound": "hbm", "achieved": abytes / (ms / 1e3) / 1e9, "peak": peak,
+                     "unit": "GB/s", "frac": abytes / (ms / 1e3) / 1e9 / peak, "traffic": None,
+                     "peak_source": peak_src, "kernel": "whole step (solve + sharded SpMV)"},
+        "e2e": {"value": 1.0 / e2e_s, "unit": UNIT, "h2d_bytes_per_step": 8 * n,
+                "d2h_bytes_per_step": 8 * n, "ms_per_step": e2e_s * 1e3},
+        "clocks": clk.summary(),
+    }
+
+
 def cpu_baseline(cfg, M, vals, vin):
     from oracle.oracle import Reference
     T = cpu_threads()
@@ -519,6 +610,8 @@ def main():
     ap.add_argument("--size", type=int, default=None, help="grid side / n override (testing)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-extras", action="store_true")
+    ap.add_argument("--shard-spmv", action="store_true",
+                    help="config 1 only: solve on rank 0, SpMV rows sharded over ranks")
     args = ap.parse_args()
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")
@@ -526,7 +619,14 @@ def main():
         return  # the reference arm runs on rank 0 only
     D = Dist() if args.impl == "ours" else _Solo()
     try:
-        line = run_reference(args, D) if args.impl == "reference" else run_ours(args, D)
+        if args.impl == "reference":
+            line = run_reference(args, D)
+        elif args.shard_spmv:
+            if args.config != 1:
+                raise SystemExit("--shard-spmv applies to --config 1")
+            line = run_sharded(args, D)
+        else:
+            line = run_ours(args, D)
         if D.rank == 0 and line is not None:
             print(json.dumps(line), flush=True)
     finally:

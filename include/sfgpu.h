@@ -160,6 +160,18 @@ sfg_status sfg_execute_unfused(sfg_plan* plan);
  * input vector). */
 sfg_status sfg_execute_batch(sfg_plan* plan, int32_t nsteps, const double* const* vin_host,
                              double* const* out_host);
+/* Kernel 1 alone (which = 1) or kernel 2 alone (which = 2, reading kernel
+ * 1's outputs from the previous call) -- the two halves of the unfused
+ * comparator, for callers that move data between them (e.g. the row-sharded
+ * SpMV of config 1 across GPUs). */
+sfg_status sfg_execute_kernel(sfg_plan* plan, int32_t which);
+/* y[r - r0] = sum_p A(r, col_p) x[col_p] for r in [r0, r1) (x indexed by
+ * absolute column, y by row within the shard), in ascending column
+ * order (the order in which spmv_csc_col, kernels.hpp:162-168, accumulates
+ * y_r: bit-identical with combo 4's kernel 2) over the plan's CSR of A
+ * (combos 2, 3, 4, 6; nsys 1).  x and y are device pointers. */
+sfg_status sfg_spmv_rows(sfg_plan* plan, int32_t r0, int32_t r1, const double* x_device,
+                         double* y_device);
 /* Waits for the plan stream; returns SFG_ERR_FACTORIZATION on breakdown. */
 sfg_status sfg_synchronize(sfg_plan* plan);
 /* collect_outputs (kernels.hpp:585-608) for every system, system-major,

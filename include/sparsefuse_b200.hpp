@@ -439,6 +439,20 @@ inline ExecStats execute_unfused(KernelState& st, Index /*nthreads*/ = 0) {
   return detail::finish(st, l0);
 }
 
+// One kernel of the pair alone (1 or 2): the halves of execute_unfused, for
+// callers that move data between them (config 1's row-sharded SpMV).
+inline void execute_kernel(KernelState& st, int which) {
+  detail::check(st.handle(), sfg_execute_kernel(st.handle(), which), "execute_kernel");
+}
+
+// y[0:r1-r0] = A[r0:r1, :] x on device pointers, bit-identical with combo 4's
+// kernel 2 rows (spmv_csc_col, kernels.hpp:162-168).
+inline void spmv_rows(KernelState& st, std::int32_t r0, std::int32_t r1, const double* x_device,
+                      double* y_device) {
+  detail::check(st.handle(), sfg_spmv_rows(st.handle(), r0, r1, x_device, y_device),
+                "spmv_rows");
+}
+
 // kernels.hpp:498-502: a no-op -- every execution re-initialises its outputs
 inline void reset(KernelState&) {}
 

@@ -328,6 +328,18 @@ class KernelState:
         op = (C.c_void_p * max(k, 1))(*[o.ctypes.data for o in outs])
         self._chk(self.L.sfg_execute_batch(self.h, k, vp, op), "execute_batch")
 
+    def execute_kernel(self, which: int, sync: bool = True):
+        """Kernel 1 or kernel 2 of the pair alone (sfg_execute_kernel)."""
+        if not self.inspected:
+            self.inspect()
+        self._chk(self.L.sfg_execute_kernel(self.h, which), "execute_kernel")
+        if sync:
+            self.synchronize()
+
+    def spmv_rows(self, r0: int, r1: int, x_device: int, y_device: int):
+        """y[0:r1-r0] = A[r0:r1, :] x on device pointers (sfg_spmv_rows)."""
+        self._chk(self.L.sfg_spmv_rows(self.h, r0, r1, x_device, y_device), "spmv_rows")
+
     def execute_unfused(self, sync: bool = True):
         if not self.inspected:
             self.inspect()

@@ -1217,10 +1217,13 @@ void exec_fused_impl(sfg_plan* P, cudaEvent_t kb, cudaEvent_t ke) {
 
 // The unfused comparator (execute_unfused, executor.hpp:325-383): kernel 1
 // alone, then kernel 2 alone; stream order is the barrier between them.
-void exec_unfused_impl(sfg_plan* P, cudaEvent_t kb, cudaEvent_t ke) {
+// which = 1 / 2 runs only that kernel (sfg_execute_kernel); kernel 2 alone
+// reads kernel 1's outputs from the previous call.
+void exec_unfused_impl(sfg_plan* P, cudaEvent_t kb, cudaEvent_t ke, int which = 3) {
   const int64_t nv = (int64_t)P->n * P->nsys;
   const int c = P->combo;
   const int32_t n = P->n;
+  const bool k1 = which & 1, k2 = which & 2;
   ExecArgs a = exec_args(P);
   FillRegion r1[2];
   int n1 = 0;
@@ -1228,7 +1231,8 @@ void exec_unfused_impl(sfg_plan* P, cudaEvent_t kb, cudaEvent_t ke) {
     r1[n1++] = {P->vmid.p, nv};
   else if (c == 5 || c == 6)
     r1[n1++] = {P->fac.p, P->nnzF};
-  launch_prep(r1, n1, P->counter.p, P->err.p, P->stream);
+  if (k1)
+    launch_prep(r1, n1, P->counter.p, P->err.p, P->stream);
   SFG_CUDA(cudaEventRecord(kb, P->stream));
   if (P->use_ell || P->use_ws) {
     EllArgs e = ell_args(P);
@@ -1238,73 +1242,105 @@ void exec_unfused_impl(sfg_plan* P, cudaEvent_t kb, cudaEvent_t ke) {
       else
         launch_chain_ell(x, P->ell_chn, P->stream);
     };
-    e.seg_begin = 0;
-    e.seg_end = P->ch_f.nbatch;
-    launch(e);
-    FillRegion r2[1] = {{P->vout.p, nv}};
-    launch_prep(r2, 1, P->counter.p, nullptr, P->stream);
-    e.seg_begin = P->ch_f.nbatch;
-    e.seg_end = P->ch_f.nbatch + P->ch_b.nbatch;
-    launch(e);
+    if (k1) {
+      e.seg_begin = 0;
+      e.seg_end = P->ch_f.nbatch;
+      launch(e);
+    }
+    if (k2) {
+      FillRegion r2[1] = {{P->vout.p, nv}};
+      launch_prep(r2, 1, P->counter.p, nullptr, P->stream);
+      e.seg_begin = P->ch_f.nbatch;
+      e.seg_end = P->ch_f.nbatch + P->ch_b.nbatch;
+      launch(e);
+    }
     SFG_CUDA(cudaEventRecord(ke, P->stream));
     return;
   }
   if (P->use_mline) {
     MLineArgs m = mline_args(P);
-    m.seg_begin = 0;
-    m.seg_end = m.f_ngroup;
-    launch_mline(m, P->stream);
-    FillRegion r2[1] = {{P->vout.p, nv}};
-    launch_prep(r2, 1, P->counter.p, nullptr, P->stream);
-    m.seg_begin = m.f_ngroup;
-    m.seg_end = m.f_ngroup + m.b_ngroup;
-    launch_mline(m, P->stream);
+    if (k1) {
+      m.seg_begin = 0;
+      m.seg_end = m.f_ngroup;
+      launch_mline(m, P->stream);
+    }
+    if (k2) {
+      FillRegion r2[1] = {{P->vout.p, nv}};
+      launch_prep(r2, 1, P->counter.p, nullptr, P->stream);
+      m.seg_begin = m.f_ngroup;
+      m.seg_end = m.f_ngroup + m.b_ngroup;
+      launch_mline(m, P->stream);
+    }
     SFG_CUDA(cudaEventRecord(ke, P->stream));
     return;
   }
   if (P->use_chain) {
     ChainArgs b = chain_args(P);
-    b.phase = 1;
-    b.seg_begin = 0;
-    b.seg_end = P->ch_f.nbatch;
-    launch_chain(b, P->stream);
-    FillRegion r2[1];
-    int n2 = 0;
-    if (c == 1 || c == 8)
-      r2[n2++] = {P->vout.p, nv};
-    launch_prep(r2, n2, P->counter.p, nullptr, P->stream);
-    b.phase = 2;
-    if (c == 8) {
-      b.seg_begin = P->ch_f.nbatch;
-      b.seg_end = P->ch_f.nbatch + P->ch_b.nbatch;
+    if (k1) {
+      b.phase = 1;
+      b.seg_begin = 0;
+      b.seg_end = P->ch_f.nbatch;
+      launch_chain(b, P->stream);
     }
-    launch_chain(b, P->stream);
+    if (k2) {
+      FillRegion r2[1];
+      int n2 = 0;
+      if (c == 1 || c == 8)
+        r2[n2++] = {P->vout.p, nv};
+      launch_prep(r2, n2, P->counter.p, nullptr, P->stream);
+      b.phase = 2;
+      b.seg_begin = 0;
+      b.seg_end = P->ch_f.nbatch;
+      if (c == 8) {
+        b.seg_begin = P->ch_f.nbatch;
+        b.seg_end = P->ch_f.nbatch + P->ch_b.nbatch;
+      }
+      launch_chain(b, P->stream);
+    }
     SFG_CUDA(cudaEventRecord(ke, P->stream));
     return;
   }
-  a.phase = 1;
-  a.t_begin = 0;
-  a.t_end = n;
-  if (c == 7)
-    launch_dscal(a, P->stream);
-  else if (c == 3)
-    launch_dscal_csr(a, P->stream);
-  else
-    launch_main(P, a);
-  FillRegion r2[2];
-  int n2 = 0;
-  if (c == 1 || c == 8 || c == 5 || c == 6)
-    r2[n2++] = {P->vout.p, nv};
-  else if (c == 7 || c == 3)
-    r2[n2++] = {P->fac.p, P->nnzF};
-  launch_prep(r2, n2, P->counter.p, nullptr, P->stream);
-  a.phase = 2;
-  if (c == 4 || c == 8) {
-    a.t_begin = n;
-    a.t_end = 2 * (int64_t)n;
+  if (k1) {
+    a.phase = 1;
+    a.t_begin = 0;
+    a.t_end = n;
+    if (c == 7)
+      launch_dscal(a, P->stream);
+    else if (c == 3)
+      launch_dscal_csr(a, P->stream);
+    else
+      launch_main(P, a);
   }
-  launch_main(P, a);
+  if (k2) {
+    FillRegion r2[2];
+    int n2 = 0;
+    if (c == 1 || c == 8 || c == 5 || c == 6)
+      r2[n2++] = {P->vout.p, nv};
+    else if (c == 7 || c == 3)
+      r2[n2++] = {P->fac.p, P->nnzF};
+    launch_prep(r2, n2, P->counter.p, nullptr, P->stream);
+    a.phase = 2;
+    a.t_begin = 0;
+    a.t_end = n;
+    if (c == 4 || c == 8) {
+      a.t_begin = n;
+      a.t_end = 2 * (int64_t)n;
+    }
+    launch_main(P, a);
+  }
   SFG_CUDA(cudaEventRecord(ke, P->stream));
+}
+
+__global__ void spmv_rows_kernel(const int32_t* __restrict__ ptr, const int32_t* __restrict__ idx,
+                                 const double* __restrict__ val, int32_t r0, int32_t r1,
+                                 const double* __restrict__ x, double* __restrict__ y) {
+  for (int64_t r = r0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < r1;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    double acc = 0.0;
+    for (int32_t p = ptr[r]; p < ptr[r + 1]; ++p)
+      acc = __dadd_rn(acc, __dmul_rn(val[p], x[idx[p]]));
+    y[r - r0] = acc;
+  }
 }
 
 } // namespace
@@ -2169,6 +2205,41 @@ sfg_status sfg_execute_unfused(sfg_plan* P) {
     exec_unfused_impl(P, P->ev[1], P->ev[2]);
     SFG_CUDA(cudaEventRecord(P->ev[3], P->stream));
     P->timed = true;
+    return SFG_OK;
+  });
+}
+
+sfg_status sfg_execute_kernel(sfg_plan* P, int32_t which) {
+  if (!P || (which != 1 && which != 2))
+    return SFG_ERR_INVALID_ARGUMENT;
+  if (!P->inspected)
+    return set_err(P, SFG_ERR_LOGIC, "sfg_inspect has not run");
+  return guarded(P, [&] {
+    DeviceScope ds(P->device);
+    LaunchScope ls(P);
+    SFG_CUDA(cudaEventRecord(P->ev[0], P->stream));
+    exec_unfused_impl(P, P->ev[1], P->ev[2], which);
+    SFG_CUDA(cudaEventRecord(P->ev[3], P->stream));
+    P->timed = true;
+    return SFG_OK;
+  });
+}
+
+sfg_status sfg_spmv_rows(sfg_plan* P, int32_t r0, int32_t r1, const double* x_device,
+                         double* y_device) {
+  if (!P || !x_device || !y_device || r0 < 0 || r1 < r0 || r1 > P->n || P->ar_ptr.p == nullptr ||
+      P->nsys != 1)
+    return SFG_ERR_INVALID_ARGUMENT;
+  return guarded(P, [&] {
+    DeviceScope ds(P->device);
+    LaunchScope ls(P);
+    if (r1 > r0) {
+      spmv_rows_kernel<<<grid_for(r1 - r0), 256, 0, P->stream>>>(P->ar_ptr.p, P->ar_idx.p,
+                                                                 P->ar_val.p, r0, r1, x_device,
+                                                                 y_device);
+      count_launch();
+      SFG_CUDA(cudaGetLastError());
+    }
     return SFG_OK;
   });
 }

@@ -491,3 +491,69 @@ def test_pcg_ic0_breakdown_reported():
     vals[M.rowidx == cols] = 1.0  # diagonal 1 with off-diagonals -1: IC0 breaks down
     with pytest.raises(sf.FactorizationError):
         sf.PCG(sf.CscMatrix(M.n, M.colptr, M.rowidx, vals))
+
+
+# ---------------------------------------------------------------------------
+# config 1 split across ranks: kernel 1 alone, then the row-sharded
+# SpMV; on one GPU the shards run back to back and must reproduce combo 4's y
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("size,world", [(64, 1), (64, 3), (512, 4), (512, 7)])
+def test_config1_sharded_spmv_matches_fused(size, world):
+    import torch
+    from paper_2111_12238_b200 import shard
+    M = sf.config_matrix(1, size=size)
+    st = sf.make_state(4, M, seed=7)
+    st.execute_fused()
+    want = st.collect_outputs()
+    n = M.n
+    st2 = sf.make_state(4, M, seed=7)
+    torch.cuda.set_device(0)
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        st2.set_stream(s.cuda_stream)  # plan and torch share one stream
+        solve, spmv = shard.plan_callbacks(st2, n)
+        x = solve()
+        ys = []
+        for r0, r1 in shard.row_shards(n, world):
+            y = torch.full((max(r1 - r0, 1),), float("nan"), dtype=torch.float64, device="cuda")
+            if r1 > r0:
+                spmv(r0, r1, x, y)
+            ys.append(y[:r1 - r0])
+        got_x = x.cpu().numpy()
+        got_y = torch.cat(ys).cpu().numpy()
+        # ShardedSpmv at world 1 is the same computation end to end
+        S = shard.ShardedSpmv(None, 0, 1, n, *shard.csr_pattern(M.colptr, M.rowidx, n),
+                              torch.device("cuda"), solve=solve, spmv=spmv)
+        y1 = S.step().cpu().numpy()
+    st2.synchronize()
+    assert np.array_equal(got_x, want[:n])
+    assert np.array_equal(got_y, want[n:2 * n])
+    assert np.array_equal(y1, want[n:2 * n])
+    st.close()
+    st2.close()
+
+
+def test_execute_kernel_two_halves_equal_unfused(golden):
+    """sfg_execute_kernel(1) then (2) == execute_unfused for every combo."""
+    M = as_sf(golden_matrix(golden, "grid10"))
+    for combo in GPU_COMBOS:
+        st = sf.make_state(combo, M, seed=7)
+        st.execute_unfused()
+        want = st.collect_outputs()
+        st2 = sf.make_state(combo, M, seed=7)
+        st2.execute_kernel(1)
+        st2.execute_kernel(2)
+        assert np.array_equal(st2.collect_outputs(), want), combo
+        st.close()
+        st2.close()
+
+
+def test_spmv_rows_rejects_bad_ranges():
+    M = sf.config_matrix(1, size=16)
+    st = sf.make_state(4, M, seed=7)
+    st.inspect()
+    with pytest.raises(Exception):
+        st.spmv_rows(5, 4, 1, 1)
+    with pytest.raises(Exception):
+        st.spmv_rows(0, M.n + 1, 1, 1)
+    st.close()
