@@ -6,6 +6,10 @@
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 
+#include <algorithm>
+#include <string>
+#include <vector>
+
 namespace sfg {
 
 namespace {
@@ -114,6 +118,77 @@ __global__ void codes_kernel(const int32_t* __restrict__ ptr, const int32_t* __r
     keys[e1] = ~0ull;
   }
   atomicMax(width, wmax);
+}
+
+
+// One warp per group, claimed in group-DAG level order.  est[g] is the
+// group's earliest start in 1/64 steps given its predecessors' (real lags,
+// which are negative where a producer row comes later in its group than the
+// consumer row in this one); key[g] = max(est[g], key[h] + 1 over
+// predecessors) is the claim priority -- est order made topological, so
+// skewed neighbours are claimed together instead of being serialised.
+// key_p1 holds key + 1 (0 = not final yet); every predecessor was claimed
+// earlier.
+__global__ void group_est_kernel(const int32_t* __restrict__ ptr, int32_t n, int dir,
+                                 const int32_t* __restrict__ cstart,
+                                 const int32_t* __restrict__ chain_of,
+                                 const int32_t* __restrict__ cskew,
+                                 const int32_t* __restrict__ code,
+                                 const int32_t* __restrict__ gorder, int32_t ng, int32_t nchain,
+                                 int32_t B, int hop, int32_t* est, int32_t* key_p1,
+                                 unsigned long long* counter) {
+  const int lane = threadIdx.x & 31;
+  for (;;) {
+    unsigned long long t = 0;
+    if (lane == 0)
+      t = atomicAdd(counter, 1ull);
+    t = __shfl_sync(FULL, t, 0);
+    if (t >= (unsigned long long)ng)
+      break;
+    const int g = gorder[t];
+    int best = 0, kbest = 0;
+    for (int b = lane; b < B; b += 32) {
+      const int c = g * B + b;
+      if (c >= nchain)
+        break;
+      const int p0 = cstart[c], len = cstart[c + 1] - p0, sk = cskew[c];
+      for (int o = 0; o < len; ++o) {
+        const int p = p0 + o;
+        const int r = dir > 0 ? p : n - 1 - p;
+        for (int e = ptr[r]; e < ptr[r + 1] - 1; ++e) {
+          const int cd = code[e];
+          if (cd < 0)
+            continue;
+          const int pj = pos_of(cd, n, dir);
+          const int cj = chain_of[pj];
+          const int h = cj / B;
+          if (h == g)
+            continue;
+          int kv;
+          while ((kv = *(volatile int32_t*)(key_p1 + h)) == 0)
+            ;
+          const int ev = *(volatile int32_t*)(est + h);
+          const int w = (cskew[cj] + (pj - cstart[cj]) - (sk + o) + 1 + hop) * 64;
+          best = ev + w > best ? ev + w : best;
+          kbest = kv > kbest ? kv : kbest; // key[h] + 1
+        }
+      }
+    }
+#pragma unroll
+    for (int o2 = 16; o2 > 0; o2 >>= 1) {
+      const int v = __shfl_xor_sync(FULL, best, o2);
+      best = v > best ? v : best;
+      const int kk = __shfl_xor_sync(FULL, kbest, o2);
+      kbest = kk > kbest ? kk : kbest;
+    }
+    if (lane == 0) {
+      *(volatile int32_t*)(est + g) = best;
+      __threadfence();
+      *(volatile int32_t*)(key_p1 + g) = (best > kbest ? best : kbest) + 1;
+      __threadfence();
+    }
+    __syncwarp();
+  }
 }
 
 // One thread per position: its step-stream record (S == 1).
@@ -692,6 +767,7 @@ __global__ void __launch_bounds__(kMThreads) k_mline1(const MLineArgs A) {
   }
 }
 
+
 template <int S, int CHN, int DX> void launch_scd(const MLineArgs& a, cudaStream_t s) {
   // single-system plans are latency-bound: one CTA per SM keeps the solve
   // warps from sharing schedulers with waiting warps (measured on C1)
@@ -783,6 +859,40 @@ void build_mline(const int32_t* ptr, const int32_t* idx, int32_t n, int dir, int
   order_by_level(level.p, ng, out.nlevels, out.gorder.p, nullptr, s);
   SFG_CUDA(cudaStreamSynchronize(s));
   out.glevel = std::move(level);
+  // SFG_GROUP_ORDER=est: claim by earliest start instead of level (an
+  // ablation; measured neutral on C5 with either multi-line executor)
+  const char* go_env = getenv("SFG_GROUP_ORDER");
+  const bool by_est = go_env && std::string(go_env) == "est";
+  if (by_est && ng > 1) {
+    DBuf<int32_t> est(ng), key(ng);
+    SFG_CUDA(cudaMemsetAsync(est.p, 0, sizeof(int32_t) * (size_t)ng, s));
+    SFG_CUDA(cudaMemsetAsync(key.p, 0, sizeof(int32_t) * (size_t)ng, s));
+    DBuf<unsigned long long> ctr(1);
+    SFG_CUDA(cudaMemsetAsync(ctr.p, 0, sizeof(unsigned long long), s));
+    int hop = 2;
+    if (const char* e = getenv("SFG_GROUP_HOP"))
+      hop = atoi(e);
+    int per_sm = 0;
+    SFG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, group_est_kernel, 128, 0));
+    const int64_t grid = std::min<int64_t>(((int64_t)ng + 3) / 4, (int64_t)std::max(per_sm, 1) * sm_count());
+    group_est_kernel<<<(unsigned)grid, 128, 0, s>>>(ptr, n, dir, out.cstart.p, out.chain_of.p,
+                                                   out.cskew.p, out.code.p, out.gorder.p, ng,
+                                                   out.nchain, B, hop, est.p, key.p, ctr.p);
+    count_launch();
+    SFG_CUDA(cudaGetLastError());
+    std::vector<int32_t> hk((size_t)ng), he((size_t)ng);
+    SFG_CUDA(cudaMemcpyAsync(hk.data(), key.p, sizeof(int32_t) * (size_t)ng, cudaMemcpyDeviceToHost, s));
+    SFG_CUDA(cudaMemcpyAsync(he.data(), est.p, sizeof(int32_t) * (size_t)ng, cudaMemcpyDeviceToHost, s));
+    SFG_CUDA(cudaStreamSynchronize(s));
+    int32_t kmax = 0, emax = 0;
+    for (size_t g = 0; g < hk.size(); ++g) {
+      kmax = std::max(kmax, hk[g]);
+      emax = std::max(emax, he[g]);
+    }
+    order_by_level(key.p, ng, kmax + 1, out.gorder.p, nullptr, s);
+    SFG_CUDA(cudaStreamSynchronize(s));
+    out.est_steps = emax / 64;
+  }
   // longest group (diagnostics)
   std::vector<int32_t> hs((size_t)ng);
   SFG_CUDA(cudaMemcpyAsync(hs.data(), out.gsteps.p, sizeof(int32_t) * (size_t)ng,
@@ -835,6 +945,10 @@ void build_mline_stream(const int32_t* ptr, const double* val, int32_t n, int di
 void launch_mline(const MLineArgs& a, cudaStream_t s) {
   if (a.seg_end <= a.seg_begin)
     return;
+  if (a.use_msys) {
+    launch_msys(a, s);
+    return;
+  }
   if (a.S == 1 && a.use_stream) {
     auto kern = a.stream_ch <= 2 ? k_mline1<2> : k_mline1<4>;
     const size_t smem = (size_t)(kMThreads / 32) *

@@ -78,6 +78,7 @@ struct sfg_plan {
   DBuf<unsigned long long> trace;  // SFG_TRACE diagnostics
   // multi-chain warp executor (combos 1, 8; default)
   bool use_mline = false;
+  bool use_msys = false; // k_msys over the B = 32 layouts (batched solves)
   MLineLayout ml_f, ml_b;
   // warp-per-task factorization executors (combos 5, 6, 7)
   bool use_warpfac = false;
@@ -681,8 +682,34 @@ void do_inspect(sfg_plan* P) {
   // executor choice: the multi-chain warp executor for single-system solve
   // pairs (latency-bound: in-warp dependencies go through shared memory),
   // the chain executor for batched systems; SFG_EXECUTOR overrides
-  const bool want_mline = (ex ? std::string(ex) == "mline" : P->nsys == 1) || combo == 2;
-  if (want_mline && (combo == 1 || combo == 2 || combo == 4 || combo == 8)) {
+  bool want_msys = ex && std::string(ex) == "msys" && P->nsys >= 2 && P->nsys % 2 == 0 &&
+                   (combo == 1 || combo == 8);
+  if (want_msys) { // one chain per lane, system pairs (msys.cu); falls back to chains
+    int32_t max_len = 1 << 20;
+    if (const char* e = getenv("SFG_CHAIN_MAX"))
+      max_len = atoi(e);
+    build_mline(P->lr_ptr.p, P->lr_idx.p, n, +1, 1, max_len, P->ml_f, s);
+    bool ok = build_msys(P->lr_ptr.p, P->lr_val.p, n, +1, P->nsys, P->ml_f, s);
+    if (ok && combo == 8) {
+      build_mline(P->lt_ptr.p, P->lt_idx.p, n, -1, 1, max_len, P->ml_b, s);
+      ok = build_msys(P->lt_ptr.p, P->lt_val.p, n, -1, P->nsys, P->ml_b, s);
+    }
+    if (ok && combo == 8 && (P->ml_f.ech != P->ml_b.ech || P->ml_f.lch != P->ml_b.lch))
+      ok = false; // one kernel instantiation serves both segments
+    if (ok) {
+      P->use_mline = true;
+      P->use_msys = true;
+    } else {
+      P->ml_f = MLineLayout{};
+      P->ml_b = MLineLayout{};
+      want_msys = false;
+    }
+  }
+  const bool want_mline =
+      !P->use_msys && ((ex ? std::string(ex) == "mline" : P->nsys == 1) || combo == 2);
+  if (P->use_msys) {
+    // layouts built above
+  } else if (want_mline && (combo == 1 || combo == 2 || combo == 4 || combo == 8)) {
     int32_t max_len = 1 << 20;
     if (const char* e = getenv("SFG_CHAIN_MAX"))
       max_len = atoi(e);
@@ -691,26 +718,32 @@ void do_inspect(sfg_plan* P) {
       build_mline(P->lt_ptr.p, P->lt_idx.p, n, -1, P->nsys, max_len, P->ml_b, s);
     P->use_mline = true;
     const char* se = getenv("SFG_MLINE_STREAM");
-    if (P->nsys == 1 && !(se && std::string(se) == "0")) { // step streams (k_mline1)
+    if (P->nsys == 1 && !P->use_msys && !(se && std::string(se) == "0")) { // step streams (k_mline1)
       build_mline_stream(P->lr_ptr.p, P->lr_val.p, n, +1, P->ml_f, s);
       if (combo == 8)
         build_mline_stream(P->lt_ptr.p, P->lt_val.p, n, -1, P->ml_b, s);
     }
+  } else if (combo == 1 || combo == 4 || combo == 8) {
+    P->use_chain = !legacy;
+  }
+  if (P->use_mline) {
     if (getenv("SFG_MLINE_STATS")) {
       for (const MLineLayout* L : {&P->ml_f, &P->ml_b})
         if (L->nchain > 0)
-          fprintf(stderr, "mline dir=%d nchain=%d ngroup=%d levels=%d max_steps=%d width=%d\n",
-                  L->dir, L->nchain, L->ngroup, L->nlevels, L->max_steps, L->CHN);
+          fprintf(stderr, "mline dir=%d nchain=%d ngroup=%d levels=%d max_steps=%d est_steps=%d width=%d%s\n",
+                  L->dir, L->nchain, L->ngroup, L->nlevels, L->max_steps, L->est_steps, L->CHN,
+                  P->use_msys ? (" msys ech=" + std::to_string(L->ech) + " lch=" +
+                                 std::to_string(L->lch)).c_str()
+                              : "");
     }
     if (getenv("SFG_TRACE")) {
       P->trace_tiles = 4;
-      const int64_t items = (int64_t)P->ml_f.ngroup + (n + 31) / 32 +
-                            (combo == 8 ? P->ml_b.ngroup : P->ml_f.ngroup);
+      const int64_t items = ((int64_t)P->ml_f.ngroup + (n + 31) / 32 +
+                             (combo == 8 ? P->ml_b.ngroup : P->ml_f.ngroup)) *
+                            (P->use_msys ? P->nsys / 2 : 1);
       P->trace.alloc(items * 4);
       SFG_CUDA(cudaMemsetAsync(P->trace.p, 0, sizeof(unsigned long long) * items * 4, s));
     }
-  } else if (combo == 1 || combo == 4 || combo == 8) {
-    P->use_chain = !legacy;
   }
   if (!legacy && (combo == 5 || combo == 7)) {
     build_ic0_updates(P->lc_ptr.p, P->lc_idx.p, P->rv_ptr.p, P->rv_col.p, P->rv_pos.p, n,
@@ -839,6 +872,13 @@ MLineArgs mline_args(sfg_plan* P) {
   a.trace = P->trace.p;
   a.use_stream = P->ml_f.stream && L2.stream && P->ml_f.sch == L2.sch;
   a.stream_ch = P->ml_f.sch;
+  a.use_msys = P->use_msys;
+  a.ech = P->ml_f.ech;
+  a.lch = P->ml_f.lch;
+  a.f_mrec = P->ml_f.mrec.p;
+  a.b_mrec = L2.mrec.p;
+  a.f_mval = P->ml_f.mval.p;
+  a.b_mval = L2.mval.p;
   a.f_sofs = P->ml_f.sofs.p;
   a.f_srow = P->ml_f.srow.p;
   a.f_scode = P->ml_f.scode.p;
@@ -851,6 +891,11 @@ MLineArgs mline_args(sfg_plan* P) {
     a.sleep_ns = (unsigned)atoi(e);
   if (const char* e = getenv("SFG_MLINE_DX"))
     a.lookahead = atoi(e);
+  if (P->use_msys) { // k_msys: L2 prefetch distance beyond the record distance
+    a.lookahead = 0;
+    if (const char* e = getenv("SFG_MSYS_PF"))
+      a.lookahead = atoi(e);
+  }
   if (const char* e = getenv("SFG_BLOCKS_PER_SM"))
     a.blocks_per_sm = atoi(e);
   return a;
@@ -1449,11 +1494,12 @@ sfg_status sfg_plan_destroy(sfg_plan* P) {
       cudaStreamSynchronize(P->stream);
     if (P->trace.p && P->use_mline) {
       // SFG_TRACE=<path>: {items, 4, fwd items, data[items*4]} (see MLineArgs::trace)
-      const int64_t items = (int64_t)P->ml_f.ngroup + (P->combo == 8 ? P->ml_b.ngroup : P->ml_f.ngroup);
+      const int64_t items = ((int64_t)P->ml_f.ngroup + (P->combo == 8 ? P->ml_b.ngroup : P->ml_f.ngroup)) *
+                            (P->use_msys ? P->nsys / 2 : 1);
       std::vector<unsigned long long> h((size_t)(items * 4));
       cudaMemcpy(h.data(), P->trace.p, sizeof(unsigned long long) * h.size(), cudaMemcpyDeviceToHost);
       if (FILE* f = fopen(getenv("SFG_TRACE"), "wb")) {
-        const int64_t hdr[3] = {items, 4, P->ml_f.ngroup};
+        const int64_t hdr[3] = {items, 4, P->ml_f.ngroup * (P->use_msys ? P->nsys / 2 : 1)};
         fwrite(hdr, sizeof(hdr), 1, f);
         fwrite(h.data(), sizeof(unsigned long long), h.size(), f);
         fclose(f);
@@ -1626,6 +1672,11 @@ sfg_status sfg_set_values(sfg_plan* P, const double* values_host) {
       build_mline_stream(P->lr_ptr.p, P->lr_val.p, n, +1, P->ml_f, s);
       if (c == 8)
         build_mline_stream(P->lt_ptr.p, P->lt_val.p, n, -1, P->ml_b, s);
+    }
+    if (P->use_msys) { // so do the k_msys value records
+      refresh_msys_values(P->lr_ptr.p, P->lr_val.p, n, +1, S, P->ml_f, s);
+      if (c == 8)
+        refresh_msys_values(P->lt_ptr.p, P->lt_val.p, n, -1, S, P->ml_b, s);
     }
     if (P->use_ell || P->use_ws) { // the chain-ELL records hold copies of the values
       build_ell(P->lr_ptr.p, P->lr_idx.p, P->lr_val.p, n, S, +1, P->ell_chn, P->ch_f, P->ell_f, s);
