@@ -160,6 +160,17 @@ sfg_status sfg_execute_unfused(sfg_plan* plan);
  * input vector). */
 sfg_status sfg_execute_batch(sfg_plan* plan, int32_t nsteps, const double* const* vin_host,
                              double* const* out_host);
+/* sfg_execute_batch with a choice of what comes back per step:
+ * SFG_OUTPUTS_ALL   -- the collect_outputs layout (as sfg_execute_batch);
+ * SFG_OUTPUTS_FINAL -- kernel 2's output vector only (x of the solve pairs,
+ *                      the second solve of combos 1 and 8, y of combo 4,
+ *                      vout of combos 5 and 6), nsys*n doubles system-major:
+ *                      the iterative-solver pattern, half the device-to-host
+ *                      bytes of the solve pairs. */
+#define SFG_OUTPUTS_ALL 0
+#define SFG_OUTPUTS_FINAL 1
+sfg_status sfg_execute_batch_ex(sfg_plan* plan, int32_t nsteps, const double* const* vin_host,
+                                double* const* out_host, int32_t outputs);
 /* Kernel 1 alone (which = 1) or kernel 2 alone (which = 2, reading kernel
  * 1's outputs from the previous call) -- the two halves of the unfused
  * comparator, for callers that move data between them (e.g. the row-sharded

@@ -29,7 +29,7 @@ EXPORTS = (
     "sfg_host_free", "sfg_bench_executions", "sfg_selftest_division", "sfg_plan_create", "sfg_plan_destroy",
     "sfg_plan_set_stream", "sfg_plan_info", "sfg_set_vin", "sfg_set_values", "sfg_inspect",
     "sfg_get_dag", "sfg_get_interdep", "sfg_get_levels", "sfg_compute_reuse",
-    "sfg_get_schedule", "sfg_get_partitioning", "sfg_execute_fused", "sfg_execute_batch", "sfg_execute_kernel", "sfg_spmv_rows", "sfg_set_vin_device", "sfg_pcg_create", "sfg_pcg_solve", "sfg_pcg_plans", "sfg_pcg_destroy", "sfg_execute_unfused",
+    "sfg_get_schedule", "sfg_get_partitioning", "sfg_execute_fused", "sfg_execute_batch", "sfg_execute_batch_ex", "sfg_execute_kernel", "sfg_spmv_rows", "sfg_set_vin_device", "sfg_pcg_create", "sfg_pcg_solve", "sfg_pcg_plans", "sfg_pcg_destroy", "sfg_execute_unfused",
     "sfg_synchronize", "sfg_collect_outputs", "sfg_device_output",
     "sfg_last_error", "sfg_launch_count", "sfg_last_exec_ms", "sfg_matrix_gen",
     "sfg_matrix_dims", "sfg_matrix_copy", "sfg_matrix_free", "sfg_matrix_read_mm",
@@ -104,6 +104,9 @@ def load(path: str | None = None):
     L.sfg_get_partitioning.restype = st
     L.sfg_execute_batch.argtypes = [vp, C.c_int32, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p)]
     L.sfg_execute_batch.restype = st
+    L.sfg_execute_batch_ex.argtypes = [vp, C.c_int32, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p),
+                                       C.c_int32]
+    L.sfg_execute_batch_ex.restype = st
     L.sfg_execute_kernel.argtypes = [vp, C.c_int32]
     L.sfg_execute_kernel.restype = st
     L.sfg_spmv_rows.argtypes = [vp, C.c_int32, C.c_int32, vp, vp]

@@ -309,24 +309,27 @@ class KernelState:
         if sync:
             self.synchronize()
 
-    def execute_batch(self, vins, outs):
+    def execute_batch(self, vins, outs, final_only: bool = False):
         """len(vins) executions with new input vectors, transfers overlapped
-        with compute (sfg_execute_batch); vins[k] / outs[k] are host arrays
-        (page-locked for the overlap) of nsys*n and nsys*output_len doubles."""
+        with compute (sfg_execute_batch_ex); vins[k] / outs[k] are host arrays
+        (page-locked for the overlap) of nsys*n doubles and nsys*output_len
+        doubles -- or, with final_only, nsys*n doubles of kernel 2's output."""
         if not self.inspected:
             self.inspect()
         k = len(vins)
         if len(outs) != k:
             raise ValueError("one output buffer per input")
+        need = self.n * self.nsys if final_only else self.output_len * self.nsys
         for v in vins:
             if v.dtype != np.float64 or v.size != self.n * self.nsys or not v.flags.c_contiguous:
                 raise ValueError("vin must be contiguous float64 of nsys * n")
         for o in outs:
-            if o.dtype != np.float64 or o.size < self.output_len * self.nsys or not o.flags.c_contiguous:
-                raise ValueError("out must be contiguous float64 of nsys * output_len")
+            if o.dtype != np.float64 or o.size < need or not o.flags.c_contiguous:
+                raise ValueError(f"out must be contiguous float64 of {need} doubles")
         vp = (C.c_void_p * max(k, 1))(*[v.ctypes.data for v in vins])
         op = (C.c_void_p * max(k, 1))(*[o.ctypes.data for o in outs])
-        self._chk(self.L.sfg_execute_batch(self.h, k, vp, op), "execute_batch")
+        self._chk(self.L.sfg_execute_batch_ex(self.h, k, vp, op, 1 if final_only else 0),
+                  "execute_batch")
 
     def execute_kernel(self, which: int, sync: bool = True):
         """Kernel 1 or kernel 2 of the pair alone (sfg_execute_kernel)."""

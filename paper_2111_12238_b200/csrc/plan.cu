@@ -2152,8 +2152,13 @@ sfg_status sfg_get_partitioning(sfg_plan* P, int32_t* nspart, int64_t* nwpart,
 // is kept, so a breakdown in any step is reported like sfg_synchronize would.
 sfg_status sfg_execute_batch(sfg_plan* P, int32_t nsteps, const double* const* vin_host,
                              double* const* out_host) {
+  return sfg_execute_batch_ex(P, nsteps, vin_host, out_host, SFG_OUTPUTS_ALL);
+}
+
+sfg_status sfg_execute_batch_ex(sfg_plan* P, int32_t nsteps, const double* const* vin_host,
+                                double* const* out_host, int32_t outputs) {
   if (!P || nsteps < 0 || (nsteps > 0 && (!vin_host || !out_host)) || P->combo == 3 ||
-      P->combo == 7)
+      P->combo == 7 || (outputs != SFG_OUTPUTS_ALL && outputs != SFG_OUTPUTS_FINAL))
     return SFG_ERR_INVALID_ARGUMENT;
   if (!P->inspected)
     return set_err(P, SFG_ERR_LOGIC, "sfg_inspect has not run");
@@ -2165,7 +2170,9 @@ sfg_status sfg_execute_batch(sfg_plan* P, int32_t nsteps, const double* const* v
     const int32_t n = P->n, S = P->nsys;
     const int64_t nv = (int64_t)n * S;
     const int c = P->combo;
-    const int64_t olen = ((c == 1 || c == 2 || c == 4 || c == 8) ? 2 * (int64_t)n : P->nnzF + n) * S;
+    const bool final_only = outputs == SFG_OUTPUTS_FINAL;
+    const int64_t olen =
+        final_only ? nv : ((c == 1 || c == 2 || c == 4 || c == 8) ? 2 * (int64_t)n : P->nnzF + n) * S;
     if (!P->copy_in) {
       SFG_CUDA(cudaStreamCreateWithFlags(&P->copy_in, cudaStreamNonBlocking));
       SFG_CUDA(cudaStreamCreateWithFlags(&P->copy_out, cudaStreamNonBlocking));
@@ -2208,7 +2215,10 @@ sfg_status sfg_execute_batch(sfg_plan* P, int32_t nsteps, const double* const* v
       SFG_CUDA(cudaMemcpyAsync(P->err_hist.p + k, P->err.p, sizeof(unsigned long long),
                                cudaMemcpyDeviceToDevice, P->stream));
       SFG_CUDA(cudaStreamWaitEvent(P->stream, out_free[b], 0));
-      collect_to_device(P, P->out_stage[b].p);
+      if (final_only)
+        deinterleave(P->vout.p, n, S, P->out_stage[b].p, P->stream);
+      else
+        collect_to_device(P, P->out_stage[b].p);
       SFG_CUDA(cudaEventRecord(out_ready[b], P->stream));
       SFG_CUDA(cudaStreamWaitEvent(P->copy_out, out_ready[b], 0));
       SFG_CUDA(cudaMemcpyAsync(out_host[k], P->out_stage[b].p, sizeof(double) * (size_t)olen,

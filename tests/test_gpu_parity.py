@@ -401,11 +401,16 @@ def test_execute_batch_equals_serial(orc, combo, nsys):
     for a in ins:
         a.array[:] = rng.uniform(-1, 1, nsys * n)
     st.execute_batch([a.array for a in ins], [o.array for o in outs])
+    finals = [abi.PinnedArray(nsys * n) for _ in range(K)]
+    st.execute_batch([a.array for a in ins], [f.array for f in finals], final_only=True)
     for k in range(K):
         st.set_vin(ins[k].array)
         st.execute_fused()
-        assert np.array_equal(outs[k].array, st.collect_outputs())
-    for a in ins + outs:
+        full = st.collect_outputs()
+        assert np.array_equal(outs[k].array, full)
+        # SFG_OUTPUTS_FINAL: kernel 2's output of every system, system-major
+        assert np.array_equal(finals[k].array, full.reshape(nsys, -1)[:, -n:].ravel())
+    for a in ins + outs + finals:
         a.free()
 
 
