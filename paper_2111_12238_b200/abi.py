@@ -12,7 +12,8 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libsfgpu.so")
+# SFG_LIB: an alternative build of the same library (A/B measurements)
+LIB_PATH = os.environ.get("SFG_LIB") or os.path.join(HERE, "libsfgpu.so")
 
 SFG_OK = 0
 SFG_ERR_FACTORIZATION = 1

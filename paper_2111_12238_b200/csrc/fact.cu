@@ -178,15 +178,34 @@ __global__ void __launch_bounds__(kFBlock) k_ic0_warp(const ExecArgs A,
   const int src = COMBO == 5 ? 0 : ((A.phase & 1) ? 1 : 2);
   const int fac_kernel = COMBO == 5 ? 1 : 2;
   const unsigned cap = A.sleep_cap;
+  // next task claimed and its column header loaded during this one (see
+  // k_ilu0_warp)
+  unsigned long long nb = 0;
+  if (lane == 0)
+    nb = atomicAdd(A.counter, 1ull);
+  long long c = (long long)__shfl_sync(FULL, nb, 0);
+  int k_nx = 0, c0_nx = 0, c1_nx = 0, q0_nx = 0, q1_nx = 0;
+  auto header = [&]() {
+    k_nx = __ldg(A.order + A.t_begin + c);
+    c0_nx = __ldg(A.lc_ptr + k_nx);
+    c1_nx = __ldg(A.lc_ptr + k_nx + 1);
+    if (do_solve) {
+      q0_nx = __ldg(A.rv_ptr + k_nx);
+      q1_nx = __ldg(A.rv_ptr + k_nx + 1);
+    }
+  };
+  if (c < total)
+    header();
   for (;;) {
-    const long long c = claim_tickets(A.counter, 1);
     if (c >= total)
       break;
-    const int k = __ldg(A.order + A.t_begin + c);
-    const int c0 = __ldg(A.lc_ptr + k);
-    const int m = __ldg(A.lc_ptr + k + 1) - c0;
-    const int q0 = __ldg(A.rv_ptr + k);
-    const int q1 = __ldg(A.rv_ptr + k + 1);
+    const int k = k_nx;
+    const int c0 = c0_nx;
+    const int m = c1_nx - c0;
+    const int q0 = q0_nx;
+    const int q1 = q1_nx;
+    if (lane == 0)
+      nb = atomicAdd(A.counter, 1ull);
     // the solve's first 32 operands L(k,j), x_j: loads in flight during the
     // factorization of column k
     unsigned long long wl = 0, wx = 0;
@@ -273,6 +292,9 @@ __global__ void __launch_bounds__(kFBlock) k_ic0_warp(const ExecArgs A,
         publish_f64(A.vout + k, __ddiv_rn(acc2, lkk));
       }
     }
+    c = (long long)__shfl_sync(FULL, nb, 0);
+    if (c < total)
+      header();
   }
 }
 
@@ -297,13 +319,28 @@ __global__ void __launch_bounds__(kFBlock) k_ilu0_warp(const ExecArgs A,
   const int src = COMBO == 6 ? 0 : ((A.phase & 1) ? 1 : 2);
   const int fac_kernel = COMBO == 6 ? 1 : 2;
   const unsigned cap = A.sleep_cap;
+  // The next task is claimed while this one runs and its row header is
+  // loaded then, so a task starts with its per-lane loads instead of three
+  // dependent round trips (claim, order, row pointers).  Progress holds: the
+  // lowest unfinished ticket is always some warp's current task.
+  unsigned long long nb = 0;
+  if (lane == 0)
+    nb = atomicAdd(A.counter, 1ull);
+  long long c = (long long)__shfl_sync(FULL, nb, 0);
+  int i_nx = 0, r0_nx = 0, r1_nx = 0;
+  if (c < total) {
+    i_nx = __ldg(A.order + A.t_begin + c);
+    r0_nx = __ldg(A.ar_ptr + i_nx);
+    r1_nx = __ldg(A.ar_ptr + i_nx + 1);
+  }
   for (;;) {
-    const long long c = claim_tickets(A.counter, 1);
     if (c >= total)
       break;
-    const int i = __ldg(A.order + A.t_begin + c);
-    const int r0 = __ldg(A.ar_ptr + i);
-    const int m = __ldg(A.ar_ptr + i + 1) - r0;
+    const int i = i_nx;
+    const int r0 = r0_nx;
+    const int m = r1_nx - r0;
+    if (lane == 0)
+      nb = atomicAdd(A.counter, 1ull);
     const int pb = r0 + lane;
     const int col = lane < m ? __ldg(A.ar_idx + pb) : 0x7fffffff;
     const bool lower = col < i;
@@ -377,6 +414,12 @@ __global__ void __launch_bounds__(kFBlock) k_ilu0_warp(const ExecArgs A,
     }
     if (do_solve && lane == 0)
       publish_f64(A.vout + i, acc2);
+    c = (long long)__shfl_sync(FULL, nb, 0);
+    if (c < total) {
+      i_nx = __ldg(A.order + A.t_begin + c);
+      r0_nx = __ldg(A.ar_ptr + i_nx);
+      r1_nx = __ldg(A.ar_ptr + i_nx + 1);
+    }
   }
 }
 
