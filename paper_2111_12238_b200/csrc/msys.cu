@@ -7,9 +7,14 @@
 // advances chain b one row per step; in-group dependencies come from a
 // shared-memory ring, everything else is staged ahead:
 //
-//   record   (row, dependency codes)       bulk copy, kDR steps ahead
-//   values   (one pre-arranged record)     bulk copy, kDV steps ahead
+//   record   (row, dependency codes)       cp.async 16 B, kDR steps ahead
+//   values   (one pre-arranged record)     cp.async 16 B, kDV steps ahead
 //   x words  (external dependencies, rhs)  cp.async 16 B, kDX steps ahead
+//
+// (optionally the record and values are prefetched HBM -> L2 further ahead,
+// SFG_MSYS_PF steps beyond kDR).  Measured on config 5 this executor is
+// slower than the chain executor -- see DESIGN.md section 4 -- and stays an
+// opt-in ablation.
 //
 // Each row's dependencies (reference summation order) are split at inspection
 // into an EARLY prefix that holds only external dependencies and a LATE
@@ -34,34 +39,6 @@ constexpr int kQR = kDR + 1, kQV = kDV + 1, kQX = kDX + 1;
 
 __device__ __forceinline__ unsigned saddr(const void* p) {
   return (unsigned)__cvta_generic_to_shared(p);
-}
-__device__ __forceinline__ void mb_init(unsigned long long* bar, unsigned count) {
-  asm volatile("mbarrier.init.shared.b64 [%0], %1;" ::"r"(saddr(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mb_arrive(unsigned long long* bar) {
-  asm volatile("mbarrier.arrive.shared.b64 _, [%0];" ::"r"(saddr(bar)) : "memory");
-}
-__device__ __forceinline__ void mb_arrive_tx(unsigned long long* bar, unsigned bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(saddr(bar)), "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mb_wait(unsigned long long* bar, unsigned parity) {
-  asm volatile(
-      "{\n"
-      ".reg .pred P1;\n"
-      "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared.b64 P1, [%0], %1;\n"
-      "@!P1 bra WAIT_%=;\n"
-      "}\n" ::"r"(saddr(bar)),
-      "r"(parity)
-      : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes,
-                                         unsigned long long* bar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, "
-               "[%3];" ::"r"(saddr(dst)),
-               "l"(src), "r"(bytes), "r"(saddr(bar))
-               : "memory");
 }
 // 16-byte copy with zero fill: bytes = 0 writes zeros and reads nothing
 __device__ __forceinline__ void cp16z(void* dst, const void* src, unsigned bytes) {
@@ -92,7 +69,6 @@ template <int ECH, int LCH> struct alignas(16) MsWarp {
   unsigned long long x[kQX][32][K::NE][2];
   unsigned long long rhs[kQX][32][2];
   double ring[kRing][32][2];
-  unsigned long long barR[kQR], barV[kQV];
 };
 
 template <int ECH, int LCH>
@@ -104,15 +80,7 @@ __global__ void __launch_bounds__(32) k_msys(const MLineArgs A) {
   const int lane = threadIdx.x & 31;
   const int S = A.S;
   const int NP = S / 2;
-  if (lane == 0) {
-    for (int k = 0; k < kQR; ++k)
-      mb_init(&W.barR[k], 32);
-    for (int k = 0; k < kQV; ++k)
-      mb_init(&W.barV[k], 32);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncwarp();
-  uint32_t uR = 0, uV = 0; // barrier uses so far (one per step per item)
+  uint32_t uR = 0, uV = 0; // steps staged so far: the record / value slot of a step
   const int64_t total = (int64_t)(A.seg_end - A.seg_begin) * NP;
   for (;;) {
     unsigned long long w0 = 0;
