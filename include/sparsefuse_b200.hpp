@@ -453,6 +453,21 @@ inline void spmv_rows(KernelState& st, std::int32_t r0, std::int32_t r1, const d
                 "spmv_rows");
 }
 
+// K executions with new right-hand sides (vin[k]: nsys*n doubles), transfers
+// overlapped with compute (sfg_execute_batch_ex).  out[k] receives the
+// collect_outputs layout (nsys*output_len doubles) or, with final_only,
+// kernel 2's output only (nsys*n doubles).  Page-locked buffers
+// (sfg_host_alloc) give the overlap; any host memory is correct.
+inline void execute_batch(KernelState& st, const std::vector<const double*>& vin,
+                          const std::vector<double*>& out, bool final_only = false) {
+  if (vin.size() != out.size())
+    throw std::invalid_argument("one output buffer per input");
+  detail::check(st.handle(),
+                sfg_execute_batch_ex(st.handle(), (std::int32_t)vin.size(), vin.data(), out.data(),
+                                     final_only ? SFG_OUTPUTS_FINAL : SFG_OUTPUTS_ALL),
+                "execute_batch");
+}
+
 // kernels.hpp:498-502: a no-op -- every execution re-initialises its outputs
 inline void reset(KernelState&) {}
 

@@ -4,6 +4,7 @@
 // execute -> collect_outputs, checked bit for bit against the C oracle
 // (oracle/sf_oracle.c, itself pinned to the reference's golden vectors).
 // Without a device it checks that make_state refuses to run (no CPU fallback).
+#include <algorithm>
 #include <cstdio>
 #include <cstring>
 #include <vector>
@@ -124,6 +125,21 @@ int main(int argc, char** argv) {
     sf::reset(st);
     sf::execute_unfused(st);
     CHECK(sf::collect_outputs(st) == want);
+    // the two halves of the unfused comparator
+    sf::execute_kernel(st, 1);
+    sf::execute_kernel(st, 2);
+    CHECK(sf::collect_outputs(st) == want);
+    if (combo != 3 && combo != 7) {
+      // batched executions, both output modes, equal to the single run
+      const std::vector<double> b = sf::gen_vector(M.nrows, 7);
+      std::vector<double> all(2 * want.size()), fin(2 * (size_t)M.nrows);
+      sf::execute_batch(st, {b.data(), b.data()}, {all.data(), all.data() + want.size()});
+      sf::execute_batch(st, {b.data(), b.data()}, {fin.data(), fin.data() + M.nrows}, true);
+      for (int k = 0; k < 2; ++k) {
+        CHECK(std::equal(want.begin(), want.end(), all.begin() + (long)k * want.size()));
+        CHECK(std::equal(want.end() - M.nrows, want.end(), fin.begin() + (long)k * M.nrows));
+      }
+    }
     std::printf("combo %d: %zu outputs bit-exact, %lld launches\n", combo, want.size(),
                 (long long)es.launches);
   }
