@@ -249,10 +249,41 @@ __global__ void __launch_bounds__(kFBlock) k_ic0_warp(const ExecArgs A,
             ws[e] = ld_relaxed_u64(A.fac + ps[e]);
             wk[e] = ld_relaxed_u64(A.fac + pl[e]);
           }
+        if constexpr (COMBO == 5) {
+          // re-poll every still-unpublished word of the batch together (one
+          // round trip per pass), so a word published while an earlier one
+          // was awaited costs no extra trip: C2 0.53 -> 0.48 ms.  On C4's
+          // long critical path (many warps waiting) the extra polling traffic
+          // costs more than it saves (11.9 -> 13.4 ms), so COMBO 7 awaits
+          // the words one at a time.
+          for (;;) {
+            bool pending = false;
 #pragma unroll
-        for (int e = 0; e < CHU; ++e)
-          if (e < cnt)
-            acc = fsub_mul(acc, resolve(wk[e], A.fac + pl[e], cap), resolve(ws[e], A.fac + ps[e], cap));
+            for (int e = 0; e < CHU; ++e)
+              pending |= e < cnt && (is_sent_hi(ws[e]) || is_sent_hi(wk[e]));
+            if (!pending)
+              break;
+#pragma unroll
+            for (int e = 0; e < CHU; ++e)
+              if (e < cnt) {
+                if (is_sent_hi(ws[e]))
+                  ws[e] = ld_relaxed_u64(A.fac + ps[e]);
+                if (is_sent_hi(wk[e]))
+                  wk[e] = ld_relaxed_u64(A.fac + pl[e]);
+              }
+          }
+#pragma unroll
+          for (int e = 0; e < CHU; ++e)
+            if (e < cnt)
+              acc = fsub_mul(acc, __longlong_as_double((long long)wk[e]),
+                             __longlong_as_double((long long)ws[e]));
+        } else {
+#pragma unroll
+          for (int e = 0; e < CHU; ++e)
+            if (e < cnt)
+              acc = fsub_mul(acc, resolve(wk[e], A.fac + pl[e], cap),
+                             resolve(ws[e], A.fac + ps[e], cap));
+        }
       }
       double l0 = 0.0;
       if (lane == 0) {
@@ -380,11 +411,26 @@ __global__ void __launch_bounds__(kFBlock) k_ilu0_warp(const ExecArgs A,
       for (int e = 0; e < kMaxIluUpd; ++e)
         if (e < nu)
           wu[e] = ld_relaxed_u64(A.fac + sq[e]);
+      // all of this lane's words re-polled together until published
+      for (;;) {
+        bool pending = dk >= 0 && is_sent_hi(wp);
+#pragma unroll
+        for (int e = 0; e < kMaxIluUpd; ++e)
+          pending |= e < nu && is_sent_hi(wu[e]);
+        if (!pending)
+          break;
+        if (dk >= 0 && is_sent_hi(wp))
+          wp = ld_relaxed_u64(A.fac + dk);
+#pragma unroll
+        for (int e = 0; e < kMaxIluUpd; ++e)
+          if (e < nu && is_sent_hi(wu[e]))
+            wu[e] = ld_relaxed_u64(A.fac + sq[e]);
+      }
       double uv[kMaxIluUpd];
 #pragma unroll
       for (int e = 0; e < kMaxIluUpd; ++e)
-        uv[e] = e < nu ? resolve(wu[e], A.fac + sq[e], cap) : 0.0;
-      const double piv = dk >= 0 ? resolve(wp, A.fac + dk, cap) : 0.0;
+        uv[e] = e < nu ? __longlong_as_double((long long)wu[e]) : 0.0;
+      const double piv = dk >= 0 ? __longlong_as_double((long long)wp) : 0.0;
       const double rcp = __drcp_rn(piv);
       const double xk = do_solve && lower ? resolve(wx, A.vout + col, cap) : 0.0;
       for (int t = 0; t < nl; ++t) {
