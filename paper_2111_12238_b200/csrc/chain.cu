@@ -643,6 +643,11 @@ __global__ void __launch_bounds__(kThreads, 2) k_chain_sm(const ChainArgs A) {
         for (int a = 0; a < CHN; ++a)
           if (a < m)
             nidx2[a] = __ldg(ib + a);
+        // the row's values (entries nb2 .. ne2, S doubles each) HBM -> L2
+        // now, so stage C's copies of them one iteration later hit L2
+        const int lines = ((ne2 - nb2 + 1) * S * 8 + 127) >> 7;
+        if (s < lines)
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(val + (size_t)nb2 * S + s * 16));
       }
       // stage C: tile t+1 -> smem buffer (t+1)&1 by 16-byte async copies
       StageBuf<S, G, CHN>& nb = wbuf[(t + 1) & 1];
