@@ -543,17 +543,21 @@ __device__ __forceinline__ void cp_async_wait1() {
   asm volatile("cp.async.wait_group 1;" ::: "memory");
 }
 
-template <int S, int G, int CHN> struct StageBuf {
+// X2 (fused combo 1): the second solve's words x2[idx] are staged with the
+// first's, so both passes of a tile share the staged values of L.
+template <int S, int G, int CHN, bool X2 = false> struct StageBuf {
   double v[G][CHN][S];
   unsigned long long x[G][CHN][S];
+  unsigned long long x2[X2 ? G : 1][X2 ? CHN : 1][S];
 };
 
 template <int S, int G, int CHN, int COMBO>
-__global__ void __launch_bounds__(kThreads, 2) k_chain_sm(const ChainArgs A) {
+__global__ void __launch_bounds__(kThreads, COMBO == 1 ? 1 : 2) k_chain_sm(const ChainArgs A) {
   static_assert(S >= 2 && S % 2 == 0, "pair copies need an even number of systems");
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  StageBuf<S, G, CHN>* wbuf =
-      reinterpret_cast<StageBuf<S, G, CHN>*>(smem_raw) + 2 * (threadIdx.x >> 5);
+  constexpr bool X2 = COMBO == 1;
+  using Buf = StageBuf<S, G, CHN, X2>;
+  Buf* wbuf = reinterpret_cast<Buf*>(smem_raw) + 2 * (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   const int k = lane / S;
   const int s = lane % S;
@@ -650,7 +654,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_chain_sm(const ChainArgs A) {
           asm volatile("prefetch.global.L2 [%0];" ::"l"(val + (size_t)nb2 * S + s * 16));
       }
       // stage C: tile t+1 -> smem buffer (t+1)&1 by 16-byte async copies
-      StageBuf<S, G, CHN>& nb = wbuf[(t + 1) & 1];
+      Buf& nb = wbuf[(t + 1) & 1];
       int nr = 0;
       bool nchained = false;
       double nd = 1.0, nvc = 0.0;
@@ -672,6 +676,8 @@ __global__ void __launch_bounds__(kThreads, 2) k_chain_sm(const ChainArgs A) {
             if (a < m) {
               cp_async_cg16(&nb.v[k][a][s], vb + a * S);
               cp_async_cg16(&nb.x[k][a][s], xb + (size_t)idx2[a] * S);
+              if (X2 && pass1 && pass2)
+                cp_async_cg16(&nb.x2[X2 ? k : 0][X2 ? a : 0][s], A.vout + s + (size_t)idx2[a] * S);
             }
         }
       }
@@ -683,7 +689,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_chain_sm(const ChainArgs A) {
         __syncwarp();
         const unsigned long long t_part = tr ? gtimer() : 0ull;
         long long c1 = 0;
-        const StageBuf<S, G, CHN>& cbuf = wbuf[t & 1];
+        const Buf& cbuf = wbuf[t & 1];
         const int r = cr;
         double x = 0.0;
         if (pass1) {
@@ -743,7 +749,35 @@ __global__ void __launch_bounds__(kThreads, 2) k_chain_sm(const ChainArgs A) {
             const double z = pass1 ? x
                                    : (crhs != SENT ? __longlong_as_double((long long)crhs)
                                                    : poll_f64(A.vmid + (size_t)r * S + s, 0));
-            acc2 = partial_sum<S>(z, cb, ceend, idx, val, A.vout, s);
+            // the words were staged with the tile (x2 beside x when fused,
+            // in x when the second solve runs alone)
+            const int m = ceend - cb < CHN ? ceend - cb : CHN;
+            unsigned long long xx[CHN];
+#pragma unroll
+            for (int a = 0; a < CHN; ++a)
+              if (a < m)
+                xx[a] = (X2 && pass1) ? cbuf.x2[X2 ? k : 0][X2 ? a : 0][s] : cbuf.x[k][a][s];
+            for (;;) {
+              bool pending = false;
+#pragma unroll
+              for (int a = 0; a < CHN; ++a)
+                pending |= a < m && is_sent_hi(xx[a]);
+              if (!pending)
+                break;
+#pragma unroll
+              for (int a = 0; a < CHN; ++a)
+                if (a < m && is_sent_hi(xx[a]))
+                  xx[a] = ld_relaxed_u64(A.vout + (size_t)cjj[a] * S + s);
+            }
+            acc2 = z;
+#pragma unroll
+            for (int a = 0; a < CHN; ++a)
+              if (a < m)
+                acc2 = __dsub_rn(acc2, __dmul_rn(cbuf.v[k][a][s],
+                                                 __longlong_as_double((long long)xx[a])));
+            for (int p = cb + CHN; p < ceend; ++p) // rows longer than the staging width
+              acc2 = __dsub_rn(acc2, __dmul_rn(__ldg(val + (size_t)p * S + s),
+                                               poll_f64(A.vout + (size_t)__ldg(idx + p) * S + s, 0)));
             if (cd == 0.0)
               report_error(A.err, 2, r, r);
           }
@@ -806,7 +840,8 @@ template <int S, int G, int COMBO> void launch_g(const ChainArgs& a, cudaStream_
   constexpr int CHN = 12;
   constexpr bool use_sm = S >= 2 && S % 2 == 0 && COMBO != 4;
   auto kern = use_sm ? k_chain_sm<(S >= 2 ? S : 2), G, CHN, COMBO> : k_chain<S, G, CHN, COMBO>;
-  const size_t smem = use_sm ? (size_t)(kThreads / 32) * 2 * sizeof(StageBuf<(S >= 2 ? S : 2), G, CHN>) : 0;
+  const size_t smem =
+      use_sm ? (size_t)(kThreads / 32) * 2 * sizeof(StageBuf<(S >= 2 ? S : 2), G, CHN, COMBO == 1>) : 0;
   if (smem > 48 * 1024)
     SFG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int per_sm = 0;
