@@ -798,13 +798,13 @@ __global__ void __launch_bounds__(kThreads, COMBO == 1 ? 1 : 2) k_chain_sm(const
           }
         }
         if (tr && lane == 0 && t < A.trace_tiles) {
-          // {claim (globaltimer ns), wait-phase cycles << 32 | carry cycles,
-          //  tile end (globaltimer ns)}
+          // {stage-D entry after the copy wait (globaltimer ns), wait-phase
+          //  cycles << 32 | carry cycles, tile end (globaltimer ns)}
           const long long c2 = clock64();
-          tr[t * 3 + 0] = t_claim;
+          tr[t * 3 + 0] = t_part;
           tr[t * 3 + 1] = ((unsigned long long)(c1 - c0) << 32) | (unsigned long long)(c2 - c1);
           tr[t * 3 + 2] = gtimer();
-          (void)t_part;
+          (void)t_claim;
         }
       }
       // rotate
