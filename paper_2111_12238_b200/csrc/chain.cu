@@ -689,6 +689,7 @@ __global__ void __launch_bounds__(kThreads, COMBO == 1 ? 1 : 2) k_chain_sm(const
         __syncwarp();
         const unsigned long long t_part = tr ? gtimer() : 0ull;
         long long c1 = 0;
+        unsigned long long t_ready = 0;
         const Buf& cbuf = wbuf[t & 1];
         const int r = cr;
         double x = 0.0;
@@ -726,8 +727,10 @@ __global__ void __launch_bounds__(kThreads, COMBO == 1 ? 1 : 2) k_chain_sm(const
             if (cd == 0.0)
               report_error(A.err, kern, bwd ? A.n - 1 - r : r, r);
           }
-          if (tr)
+          if (tr) {
             c1 = clock64();
+            t_ready = gtimer();
+          }
 #pragma unroll
           for (int kk = 0; kk < G; ++kk) {
             const double v = cchained ? __dsub_rn(acc, __dmul_rn(cvc, carry)) : acc;
@@ -798,13 +801,18 @@ __global__ void __launch_bounds__(kThreads, COMBO == 1 ? 1 : 2) k_chain_sm(const
           }
         }
         if (tr && lane == 0 && t < A.trace_tiles) {
-          // {stage-D entry after the copy wait (globaltimer ns), wait-phase
-          //  cycles << 32 | carry cycles, tile end (globaltimer ns)}
+          // {stage-D entry after the copy wait (globaltimer ns),
+          //  chain id << 44 | ns from entry to every term summed << 22 | carry
+          //  cycles, tile end (globaltimer ns)}
           const long long c2 = clock64();
+          const unsigned long long lim = (1ull << 22) - 1;
+          const unsigned long long dr = pass1 ? t_ready - t_part : 0ull;
+          const unsigned long long cc = (unsigned long long)(c2 - c1);
           tr[t * 3 + 0] = t_part;
-          tr[t * 3 + 1] = ((unsigned long long)(c1 - c0) << 32) | (unsigned long long)(c2 - c1);
+          tr[t * 3 + 1] = ((unsigned long long)c << 44) | ((dr < lim ? dr : lim) << 22) | (cc < lim ? cc : lim);
           tr[t * 3 + 2] = gtimer();
           (void)t_claim;
+          (void)c0;
         }
       }
       // rotate

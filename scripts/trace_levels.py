@@ -7,7 +7,7 @@ out = "/tmp/trace.bin"
 os.environ["SFG_TRACE"] = out
 os.environ.setdefault("SFG_TRACE_TILES", "40")
 import paper_2111_12238_b200 as sf
-M, vals = sf.config5_systems(size=None, nsys=8)
+M, vals = sf.config5_systems(size=int(os.environ.get("C5_SIZE", "0")) or None, nsys=8)
 st = sf.make_state(8, M, nsys=8, values=vals)
 st.inspect()
 for _ in range(3):
@@ -24,8 +24,8 @@ t0 = ends[valid].min()
 e = np.where(valid, ends - t0, -1).astype(np.float64) / 1e3  # us
 claim = (d[:, 0, 0].astype(np.int64) - t0) / 1e3  # stage-D entry of tile 0
 entry = np.where(valid, d[:, :, 0].astype(np.int64) - t0, -1).astype(np.float64) / 1e3
-wait = (d[:, :, 1] >> 32).astype(np.float64)
-carry = (d[:, :, 1] & 0xffffffff).astype(np.float64)
+wait = ((d[:, :, 1] >> 22) & ((1 << 22) - 1)).astype(np.float64) * 1.965  # ns -> cycles
+carry = (d[:, :, 1] & ((1 << 22) - 1)).astype(np.float64)
 dd = np.diff(np.unique(ends[valid][:200000]))
 print("globaltimer min step ns", dd[dd > 0].min() if dd.size else None)
 ntile = valid.sum(1)
