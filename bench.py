@@ -185,9 +185,12 @@ def physical_bytes(cfg: int, n: int, nnzL: int, nnzA: int, S: int) -> int:
 
 
 def kernel_name(cfg: int, combo: int, S: int) -> str:
-    return {8: f"k_chain_sm<{S},4,12,8> (fwd L + bwd L^T)", 1: f"k_chain_sm<{S},4,12,1>",
-            4: "k_chain<1,...,4> (fwd L + SpMV tails)", 5: "k_ic0_warp<5>",
-            6: "k_ilu0_warp", 7: "k_ic0_warp<7>"}.get(combo, f"combo {combo} executor")
+    if S == 1 and combo in (1, 2, 4, 8):  # single systems: multi-line step-stream executor
+        return {4: "k_mline1 (fwd L + SpMV row blocks)", 2: "k_mline1 (SpMV blocks + fwd L)"}.get(
+            combo, f"k_mline1 (combo {combo})")
+    return {8: f"k_chain_sm<{S},4,12,8> (fwd L + bwd L^T)", 1: f"k_chain_sm<{S},4,12,1> (fwd L + fwd L)",
+            5: "k_ic0_warp<5>", 6: "k_ilu0_warp<6>", 3: "k_ilu0_warp<3>",
+            7: "k_ic0_warp<7>"}.get(combo, f"combo {combo} executor")
 
 
 def lower_nnz(M) -> int:
@@ -534,6 +537,26 @@ def other_configs(args):
             rec["ner_vs_cpu_reference"] = (insp / ((cpu - ms) / 1e3)) if cpu > ms else None
         out[f"config{cfg}"] = rec
         st.close()
+    # config 5's systems under the reference's own combo 1 (fwd L -> fwd L, the
+    # pair the CPU baseline times): its joint DAG lets the second solve trail
+    # the first, so fused should beat the unfused two-launch sequence
+    S = args.systems_per_gpu
+    M, vals, vin = make_inputs(5, args.size, S, 0)
+    st = sf.make_state(1, M, seed=7, nsys=S, values=vals, vin=vin).inspect()
+    reps = 20
+    st.bench(3)
+    tot, ker = st.bench(reps)
+    st.bench(3, unfused=True)
+    ut, _ = st.bench(reps, unfused=True)
+    nnzL = lower_nnz(M)
+    byts = algorithmic_bytes(5, M.n, nnzL, M.nnz) * S
+    out["config5_fwdfwd"] = {"workload": CONFIG_NAME[5].replace("bwd L^T", "fwd L (combo 1)"),
+                             "systems": S, "value": S * reps / (tot / 1e3),
+                             "ms_per_exec": tot / reps, "kernel_ms": ker,
+                             "achieved_gbs": byts / (ker / 1e3) / 1e9,
+                             "frac": byts / (ker / 1e3) / 1e9 / peak,
+                             "unfused_ms_per_exec": ut / reps, "fused_speedup": ut / tot}
+    st.close()
     # the iterative solver the executors serve: PCG with the IC0
     # factor (combo 5) and the fused forward/backward solve (combo 8) as M^-1
     M = sf.config_matrix(2)

@@ -255,7 +255,7 @@ __global__ void __launch_bounds__(kFBlock) k_ic0_warp(const ExecArgs A,
           // was awaited costs no extra trip: C2 0.53 -> 0.48 ms.  On C4's
           // long critical path (many warps waiting) the extra polling traffic
           // costs more than it saves (11.9 -> 13.4 ms), so COMBO 7 awaits
-          // the words one at a time.
+          // the updates one at a time (below).
           for (;;) {
             bool pending = false;
 #pragma unroll
@@ -278,11 +278,32 @@ __global__ void __launch_bounds__(kFBlock) k_ic0_warp(const ExecArgs A,
               acc = fsub_mul(acc, __longlong_as_double((long long)wk[e]),
                              __longlong_as_double((long long)ws[e]));
         } else {
+          // in order; an update whose words are still out spins on both of
+          // them together, then the later stale words of the batch are
+          // re-read once (their producers may have published meanwhile), so
+          // words from the same producer cost one round trip, not one each
 #pragma unroll
           for (int e = 0; e < CHU; ++e)
-            if (e < cnt)
-              acc = fsub_mul(acc, resolve(wk[e], A.fac + pl[e], cap),
-                             resolve(ws[e], A.fac + ps[e], cap));
+            if (e < cnt) {
+              if (is_sent_hi(wk[e]) || is_sent_hi(ws[e])) {
+                do {
+                  if (is_sent_hi(wk[e]))
+                    wk[e] = ld_relaxed_u64(A.fac + pl[e]);
+                  if (is_sent_hi(ws[e]))
+                    ws[e] = ld_relaxed_u64(A.fac + ps[e]);
+                } while (is_sent_hi(wk[e]) || is_sent_hi(ws[e]));
+#pragma unroll
+                for (int f = e + 1; f < CHU; ++f)
+                  if (f < cnt) {
+                    if (is_sent_hi(wk[f]))
+                      wk[f] = ld_relaxed_u64(A.fac + pl[f]);
+                    if (is_sent_hi(ws[f]))
+                      ws[f] = ld_relaxed_u64(A.fac + ps[f]);
+                  }
+              }
+              acc = fsub_mul(acc, __longlong_as_double((long long)wk[e]),
+                             __longlong_as_double((long long)ws[e]));
+            }
         }
       }
       double l0 = 0.0;
@@ -310,8 +331,15 @@ __global__ void __launch_bounds__(kFBlock) k_ic0_warp(const ExecArgs A,
             wl = ld_relaxed_u64(A.fac + ql);
             wx = ld_relaxed_u64(A.vout + qx);
           }
-          lv = resolve(wl, A.fac + ql, cap);
-          xv = resolve(wx, A.vout + qx, cap);
+          // L(k,j) and x_j come from the same task j: await them together
+          while (is_sent_hi(wl) || is_sent_hi(wx)) {
+            if (is_sent_hi(wl))
+              wl = ld_relaxed_u64(A.fac + ql);
+            if (is_sent_hi(wx))
+              wx = ld_relaxed_u64(A.vout + qx);
+          }
+          lv = __longlong_as_double((long long)wl);
+          xv = __longlong_as_double((long long)wx);
         }
         const int cnt = min(32, q1 - qb);
         for (int t = 0; t < cnt; ++t)
@@ -411,9 +439,11 @@ __global__ void __launch_bounds__(kFBlock) k_ilu0_warp(const ExecArgs A,
       for (int e = 0; e < kMaxIluUpd; ++e)
         if (e < nu)
           wu[e] = ld_relaxed_u64(A.fac + sq[e]);
-      // all of this lane's words re-polled together until published
+      // all of this lane's words re-polled together until published; the
+      // solve's x_col (published by the same task as U(col, .)) with them
+      const bool want_x = do_solve && lower;
       for (;;) {
-        bool pending = dk >= 0 && is_sent_hi(wp);
+        bool pending = (dk >= 0 && is_sent_hi(wp)) || (want_x && is_sent_hi(wx));
 #pragma unroll
         for (int e = 0; e < kMaxIluUpd; ++e)
           pending |= e < nu && is_sent_hi(wu[e]);
@@ -421,6 +451,8 @@ __global__ void __launch_bounds__(kFBlock) k_ilu0_warp(const ExecArgs A,
           break;
         if (dk >= 0 && is_sent_hi(wp))
           wp = ld_relaxed_u64(A.fac + dk);
+        if (want_x && is_sent_hi(wx))
+          wx = ld_relaxed_u64(A.vout + col);
 #pragma unroll
         for (int e = 0; e < kMaxIluUpd; ++e)
           if (e < nu && is_sent_hi(wu[e]))
@@ -432,7 +464,7 @@ __global__ void __launch_bounds__(kFBlock) k_ilu0_warp(const ExecArgs A,
         uv[e] = e < nu ? __longlong_as_double((long long)wu[e]) : 0.0;
       const double piv = dk >= 0 ? __longlong_as_double((long long)wp) : 0.0;
       const double rcp = __drcp_rn(piv);
-      const double xk = do_solve && lower ? resolve(wx, A.vout + col, cap) : 0.0;
+      const double xk = want_x ? __longlong_as_double((long long)wx) : 0.0;
       for (int t = 0; t < nl; ++t) {
         if (lane == t) {
           if (dk < 0 || piv == 0.0)

@@ -15,6 +15,7 @@ for rep in 1 2; do
   run base "$@"
   for a in $alts; do run $a "$@"; done
 done
+kexpr=${AB_TESTS:-"config5 or multisystem or golden_outputs"}
 for a in $alts; do
-  SFG_LIB=old_lib/$a/libsfgpu.so timeout 600 python -m pytest tests/test_gpu_parity.py -m gpu -x -q -p no:cacheprovider -k "config5 or multisystem or golden_outputs" > /tmp/t.txt 2>&1; echo "$a parity rc=$? $(tail -1 /tmp/t.txt)" >> $out
+  SFG_LIB=old_lib/$a/libsfgpu.so timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_edges.py -m gpu -x -q -p no:cacheprovider -k "$kexpr" > /tmp/t.txt 2>&1; echo "$a parity rc=$? $(tail -1 /tmp/t.txt)" >> $out
 done
