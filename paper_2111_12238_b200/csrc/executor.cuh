@@ -17,6 +17,9 @@ struct ExecArgs {
   const int32_t* order = nullptr;
   int64_t t_begin = 0, t_end = 0; // ticket range of this launch
   unsigned long long* counter = nullptr;
+  // SFG_TRACE (factorization warps): per ticket {task, start, summed, fac
+  // published, solve published} (globaltimer ns), 5 words
+  unsigned long long* ftrace = nullptr;
   unsigned long long* err = nullptr;
   // L in CSR, diagonal last (trsv_csr_row, kernels.hpp:171-181)
   const int32_t* lr_ptr = nullptr;

@@ -21,6 +21,12 @@ constexpr int CHU = 8;        // IC0: updates staged per lane per batch
 constexpr int kMaxIluUpd = 8;  // ILU0: updates a lane holds in registers
 constexpr unsigned FULL = 0xffffffffu;
 
+__device__ __forceinline__ unsigned long long ftimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
 __device__ __forceinline__ double fsub_mul(double acc, double a, double b) {
   return __dsub_rn(acc, __dmul_rn(a, b));
 }
@@ -204,6 +210,11 @@ __global__ void __launch_bounds__(kFBlock) k_ic0_warp(const ExecArgs A,
     const int m = c1_nx - c0;
     const int q0 = q0_nx;
     const int q1 = q1_nx;
+    unsigned long long* const ftr = A.ftrace ? A.ftrace + (size_t)c * 5 : nullptr;
+    if (ftr && lane == 0) {
+      ftr[0] = (unsigned long long)k;
+      ftr[1] = ftimer();
+    }
     if (lane == 0)
       nb = atomicAdd(A.counter, 1ull);
     // the solve's first 32 operands L(k,j), x_j: loads in flight during the
@@ -313,10 +324,17 @@ __global__ void __launch_bounds__(kFBlock) k_ic0_warp(const ExecArgs A,
         l0 = __dsqrt_rn(acc);
       }
       lkk = __shfl_sync(FULL, l0, 0);
+      if (ftr && lane == 0)
+        ftr[2] = ftimer();
       // (a reciprocal formed after the square root and broadcast measured
       // slower than the lanes' own IEEE divisions: C4 15.5 vs 13.1 ms)
       if (lane < m)
         publish_f64(A.fac + pa, lane == 0 ? lkk : __ddiv_rn(acc, lkk));
+      if (ftr) {
+        __syncwarp();
+        if (lane == 0)
+          ftr[3] = ftimer();
+      }
     } else {
       lkk = do_solve ? poll_f64(A.fac + c0, cap) : 0.0;
     }
@@ -349,6 +367,8 @@ __global__ void __launch_bounds__(kFBlock) k_ic0_warp(const ExecArgs A,
         if (lkk == 0.0)
           report_error(A.err, 2, k, k);
         publish_f64(A.vout + k, __ddiv_rn(acc2, lkk));
+        if (ftr)
+          ftr[4] = ftimer();
       }
     }
     c = (long long)__shfl_sync(FULL, nb, 0);
@@ -398,6 +418,11 @@ __global__ void __launch_bounds__(kFBlock) k_ilu0_warp(const ExecArgs A,
     const int i = i_nx;
     const int r0 = r0_nx;
     const int m = r1_nx - r0;
+    unsigned long long* const ftr = A.ftrace ? A.ftrace + (size_t)c * 5 : nullptr;
+    if (ftr && lane == 0) {
+      ftr[0] = (unsigned long long)i;
+      ftr[1] = ftimer();
+    }
     if (lane == 0)
       nb = atomicAdd(A.counter, 1ull);
     const int pb = r0 + lane;
@@ -462,6 +487,11 @@ __global__ void __launch_bounds__(kFBlock) k_ilu0_warp(const ExecArgs A,
 #pragma unroll
       for (int e = 0; e < kMaxIluUpd; ++e)
         uv[e] = e < nu ? __longlong_as_double((long long)wu[e]) : 0.0;
+      if (ftr) {
+        __syncwarp();
+        if (lane == 0)
+          ftr[2] = ftimer();
+      }
       const double piv = dk >= 0 ? __longlong_as_double((long long)wp) : 0.0;
       const double rcp = __drcp_rn(piv);
       const double xk = want_x ? __longlong_as_double((long long)wx) : 0.0;
@@ -481,6 +511,11 @@ __global__ void __launch_bounds__(kFBlock) k_ilu0_warp(const ExecArgs A,
       }
       if (lane < m)
         publish_f64(A.fac + pb, acc);
+      if (ftr) {
+        __syncwarp();
+        if (lane == 0)
+          ftr[3] = ftimer();
+      }
     } else if (do_solve) { // unit solve alone (unfused second launch)
       double lv = 0.0, xk = 0.0;
       if (lower) {
@@ -490,8 +525,11 @@ __global__ void __launch_bounds__(kFBlock) k_ilu0_warp(const ExecArgs A,
       for (int t = 0; t < nl; ++t)
         acc2 = fsub_mul(acc2, __shfl_sync(FULL, lv, t), __shfl_sync(FULL, xk, t));
     }
-    if (do_solve && lane == 0)
+    if (do_solve && lane == 0) {
       publish_f64(A.vout + i, acc2);
+      if (ftr)
+        ftr[4] = ftimer();
+    }
     c = (long long)__shfl_sync(FULL, nb, 0);
     if (c < total) {
       i_nx = __ldg(A.order + A.t_begin + c);

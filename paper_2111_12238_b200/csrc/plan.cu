@@ -595,6 +595,8 @@ ExecArgs exec_args(sfg_plan* P) {
     a.sleep_cap = (unsigned)atoi(e);
   if (const char* e = getenv("SFG_BLOCKS_PER_SM"))
     a.blocks_per_sm = atoi(e);
+  if (P->use_warpfac && P->trace.p)
+    a.ftrace = P->trace.p;
   return a;
 }
 
@@ -755,6 +757,10 @@ void do_inspect(sfg_plan* P) {
   }
   if (!P->use_warpfac)
     P->upd = UpdateLists{};
+  if (P->use_warpfac && getenv("SFG_TRACE")) {
+    P->trace.alloc((int64_t)n * 5);
+    SFG_CUDA(cudaMemsetAsync(P->trace.p, 0, sizeof(unsigned long long) * (size_t)n * 5, s));
+  }
   if (P->use_chain) {
     if (const char* e = getenv("SFG_CHAIN_G"))
       P->tile_rows = atoi(e);
@@ -1492,7 +1498,18 @@ sfg_status sfg_plan_destroy(sfg_plan* P) {
     DeviceScope ds(P->device);
     if (P->stream)
       cudaStreamSynchronize(P->stream);
-    if (P->trace.p && P->use_mline) {
+    if (P->trace.p && P->use_warpfac) {
+      // SFG_TRACE=<path>: {tasks, 5, 0, data[tasks*5]} (see ExecArgs::ftrace)
+      const int64_t items = P->n;
+      std::vector<unsigned long long> h((size_t)(items * 5));
+      cudaMemcpy(h.data(), P->trace.p, sizeof(unsigned long long) * h.size(), cudaMemcpyDeviceToHost);
+      if (FILE* f = fopen(getenv("SFG_TRACE"), "wb")) {
+        const int64_t hdr[3] = {items, 5, 0};
+        fwrite(hdr, sizeof(hdr), 1, f);
+        fwrite(h.data(), sizeof(unsigned long long), h.size(), f);
+        fclose(f);
+      }
+    } else if (P->trace.p && P->use_mline) {
       // SFG_TRACE=<path>: {items, 4, fwd items, data[items*4]} (see MLineArgs::trace)
       const int64_t items = ((int64_t)P->ml_f.ngroup + (P->combo == 8 ? P->ml_b.ngroup : P->ml_f.ngroup)) *
                             (P->use_msys ? P->nsys / 2 : 1);
