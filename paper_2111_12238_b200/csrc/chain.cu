@@ -4,6 +4,10 @@
 #include "chain.cuh"
 #include "common.cuh"
 
+#ifndef SFG_REFRESH
+#define SFG_REFRESH 1 // re-stage a tile's dependency words before stage C (0: off, A/B builds)
+#endif
+
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 
@@ -653,6 +657,24 @@ __global__ void __launch_bounds__(kThreads, COMBO == 1 ? 1 : 2) k_chain_sm(const
         if (s < lines)
           asm volatile("prefetch.global.L2 [%0];" ::"l"(val + (size_t)nb2 * S + s * 16));
       }
+#if SFG_REFRESH
+      // re-copy the dependency words of tile t (staged one iteration ago)
+      // now, so stage D checks a snapshot taken one stage C earlier rather
+      // than a whole iteration earlier: words published in between need no
+      // re-poll round trip (C5 2.167 -> 2.144 ms kernel; the same copy at the
+      // top of the iteration 2.153 ms).  Either copy may land last; both read
+      // a word that is written once, so the slot holds the sentinel or the
+      // value.
+      if (t >= 0 && cact && copier) {
+        const int m = ceend - cb < CHN ? ceend - cb : CHN;
+        Buf& rb = wbuf[t & 1];
+#pragma unroll
+        for (int a = 0; a < CHN; ++a)
+          if (a < m)
+            cp_async_cg16(&rb.x[k][a][s], xs + s + (size_t)cjj[a] * S);
+      }
+      cp_async_commit();
+#endif
       // stage C: tile t+1 -> smem buffer (t+1)&1 by 16-byte async copies
       Buf& nb = wbuf[(t + 1) & 1];
       int nr = 0;
