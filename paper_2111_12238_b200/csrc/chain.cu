@@ -4,6 +4,17 @@
 #include "chain.cuh"
 #include "common.cuh"
 
+#ifndef SFG_CHAIN_MINB
+#define SFG_CHAIN_MINB 1 // k_chain_sm blocks per SM it is compiled for (A/B builds)
+#endif
+#ifndef SFG_CHAIN_THREADS
+// k_chain_sm block: one CTA of 12 warps per SM with up to 170 registers a
+// thread measured fastest (C5 2.144 -> 1.942 ms against 2 CTAs of 8 warps at
+// 128 registers; 8 warps 2.076, 10 warps 1.975, 13-16 warps 2.11-2.18 ms);
+// the combo-1 staging buffers of 12 warps just fit in 227 KB
+#define SFG_CHAIN_THREADS 384
+#endif
+
 #ifndef SFG_REFRESH
 #define SFG_REFRESH 1 // re-stage a tile's dependency words before stage C (0: off, A/B builds)
 #endif
@@ -17,6 +28,7 @@ namespace {
 
 constexpr unsigned FULL = 0xffffffffu;
 constexpr int kThreads = 256;
+constexpr int kSmThreads = SFG_CHAIN_THREADS;
 constexpr int CH = 16; // dependencies staged in registers per batch
 
 template <typename T> struct TmpBuf {
@@ -556,7 +568,7 @@ template <int S, int G, int CHN, bool X2 = false> struct StageBuf {
 };
 
 template <int S, int G, int CHN, int COMBO>
-__global__ void __launch_bounds__(kThreads, COMBO == 1 ? 1 : 2) k_chain_sm(const ChainArgs A) {
+__global__ void __launch_bounds__(kSmThreads, COMBO == 1 ? 1 : SFG_CHAIN_MINB) k_chain_sm(const ChainArgs A) {
   static_assert(S >= 2 && S % 2 == 0, "pair copies need an even number of systems");
   extern __shared__ __align__(16) unsigned char smem_raw[];
   constexpr bool X2 = COMBO == 1;
@@ -871,22 +883,23 @@ template <int S, int G, int COMBO> void launch_g(const ChainArgs& a, cudaStream_
   constexpr bool use_sm = S >= 2 && S % 2 == 0 && COMBO != 4;
   auto kern = use_sm ? k_chain_sm<(S >= 2 ? S : 2), G, CHN, COMBO> : k_chain<S, G, CHN, COMBO>;
   const size_t smem =
-      use_sm ? (size_t)(kThreads / 32) * 2 * sizeof(StageBuf<(S >= 2 ? S : 2), G, CHN, COMBO == 1>) : 0;
+      use_sm ? (size_t)(kSmThreads / 32) * 2 * sizeof(StageBuf<(S >= 2 ? S : 2), G, CHN, COMBO == 1>) : 0;
   if (smem > 48 * 1024)
     SFG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int per_sm = 0;
-  SFG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, smem));
+  SFG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, use_sm ? kSmThreads : kThreads, smem));
   if (per_sm < 1)
     per_sm = 1;
   if (a.blocks_per_sm > 0 && a.blocks_per_sm < per_sm)
     per_sm = a.blocks_per_sm;
   const int64_t items = a.seg_end - a.seg_begin;
-  int64_t grid = (items + (kThreads / 32) - 1) / (kThreads / 32);
+  const int threads = use_sm ? kSmThreads : kThreads;
+  int64_t grid = (items + (threads / 32) - 1) / (threads / 32);
   if (grid > (int64_t)per_sm * sm_count())
     grid = (int64_t)per_sm * sm_count();
   if (grid < 1)
     return;
-  kern<<<(unsigned)grid, kThreads, smem, s>>>(a);
+  kern<<<(unsigned)grid, threads, smem, s>>>(a);
   count_launch();
   SFG_CUDA(cudaGetLastError());
 }
