@@ -4,6 +4,7 @@
 #include "chain.cuh"
 #include "common.cuh"
 
+
 #ifndef SFG_CHAIN_MINB
 #define SFG_CHAIN_MINB 1 // k_chain_sm blocks per SM it is compiled for (A/B builds)
 #endif
@@ -709,7 +710,11 @@ __global__ void __launch_bounds__(kSmThreads, COMBO == 1 ? 1 : SFG_CHAIN_MINB) k
           for (int a = 0; a < CHN; ++a)
             if (a < m) {
               cp_async_cg16(&nb.v[k][a][s], vb + a * S);
-              cp_async_cg16(&nb.x[k][a][s], xb + (size_t)idx2[a] * S);
+              // combo 1 leaves these words to the refresh copy one stage
+              // before stage D (fwd->fwd 1.473 -> 1.408 ms; combo 8 measured
+              // 1.940 -> 2.021 ms without its early copy)
+              if (!(SFG_REFRESH && X2))
+                cp_async_cg16(&nb.x[k][a][s], xb + (size_t)idx2[a] * S);
               if (X2 && pass1 && pass2)
                 cp_async_cg16(&nb.x2[X2 ? k : 0][X2 ? a : 0][s], A.vout + s + (size_t)idx2[a] * S);
             }
