@@ -89,3 +89,49 @@ def test_batched_edge_cases(orc, nsys):
                 Ms = Csc(Mo.n, Mo.colptr, Mo.rowidx, vals[s * Mo.nnz:(s + 1) * Mo.nnz])
                 want = orc.run_sequential(combo, Ms, 7, vin=vin[s * Mo.n:(s + 1) * Mo.n])
                 assert np.array_equal(got[s], want), (name, combo, nsys, s)
+
+
+def random_lower_csc(n, per_row, span, seed):
+    """Random sparse lower-triangular pattern (no grid structure): row i gets
+    up to per_row entries drawn from [i - span, i), a dominant diagonal."""
+    rng = np.random.default_rng(seed)
+    rows, cols, vals = [], [], []
+    for i in range(n):
+        lo = max(0, i - span)
+        k = min(per_row, i - lo)
+        js = np.unique(rng.integers(lo, i, size=k)) if k > 0 else np.array([], np.int64)
+        for j in js:
+            rows.append(i)
+            cols.append(j)
+            vals.append(-rng.uniform(0.1, 1.0))
+        rows.append(i)
+        cols.append(i)
+        vals.append(float(per_row) + 1.0 + rng.uniform(0, 1))
+    rows, cols, vals = np.array(rows), np.array(cols), np.array(vals)
+    order = np.lexsort((rows, cols))
+    rows, cols, vals = rows[order], cols[order], vals[order]
+    colptr = np.zeros(n + 1, np.int64)
+    np.add.at(colptr, cols + 1, 1)
+    colptr = np.cumsum(colptr)
+    return Csc(n, colptr.astype(np.int32), rows.astype(np.int32), vals.astype(np.float64))
+
+
+# batched solves on irregular patterns: chains of every length, rows of 0 to
+# 20 dependencies (beyond the 12-term staging width), all executors' default
+@pytest.mark.parametrize("n,per_row,span,nsys", [(3000, 6, 40, 8), (2000, 20, 300, 4), (4000, 3, 5000, 16)])
+def test_batched_random_patterns(orc, n, per_row, span, nsys):
+    Mo = random_lower_csc(n, per_row, span, seed=n + per_row)
+    rng = np.random.default_rng(span)
+    vals = np.concatenate([Mo.values * (1 + 0.02 * s) for s in range(nsys)])
+    vin = rng.uniform(-1, 1, nsys * n)
+    M = sf.CscMatrix(n, Mo.colptr, Mo.rowidx, Mo.values)
+    for combo in (1, 8):
+        st = sf.make_state(combo, M, nsys=nsys, values=vals, vin=vin)
+        for _ in range(2):
+            st.execute_fused()
+            got = st.collect_outputs().reshape(nsys, -1)
+            for s in (0, nsys // 2, nsys - 1):
+                Ms = Csc(n, Mo.colptr, Mo.rowidx, vals[s * Mo.nnz:(s + 1) * Mo.nnz])
+                want = orc.run_sequential(combo, Ms, 7, vin=vin[s * n:(s + 1) * n])
+                assert np.array_equal(got[s], want), (combo, nsys, s)
+        st.close()
