@@ -12,12 +12,25 @@
 #include "common.cuh"
 #include "fact.cuh"
 
+#ifndef SFG_IC5_CHU
+// IC0 combo 5: update slots per batch.  Four (72 registers, 3 blocks per SM)
+// instead of eight (116 registers, 2 blocks): C2 0.478 -> 0.444 ms
+#define SFG_IC5_CHU 4
+#endif
+#ifndef SFG_IC5_MINB
+#define SFG_IC5_MINB 1 // blocks per SM k_ic0_warp<5> is compiled for (A/B builds)
+#endif
+
+#ifndef SFG_ILU_MINB4
+#define SFG_ILU_MINB4 3 // blocks per SM the 4-slot ILU0 warp kernel is compiled for
+#endif
+
 namespace sfg {
 
 namespace {
 
 constexpr int kFBlock = 256;
-constexpr int CHU = 8;        // IC0: updates staged per lane per batch
+constexpr int CHU_DEFAULT = 8; // IC0: updates staged per lane per batch
 constexpr int kMaxIluUpd = 8;  // ILU0: updates a lane holds in registers
 constexpr unsigned FULL = 0xffffffffu;
 
@@ -173,10 +186,11 @@ void build_lists(int32_t n, int64_t nnz, const int32_t* tptr, UpdateLists& out, 
 // applied on load (dscal_csc_col, kernels.hpp:281-286) for combo 7.
 //   src 0: column k from lc_val; 1: scaled on load; 2: pre-scaled in work.
 template <int COMBO>
-__global__ void __launch_bounds__(kFBlock) k_ic0_warp(const ExecArgs A,
+__global__ void __launch_bounds__(kFBlock, COMBO == 5 ? SFG_IC5_MINB : 1) k_ic0_warp(const ExecArgs A,
                                                       const int32_t* __restrict__ uptr,
                                                       const int32_t* __restrict__ usrc,
                                                       const int32_t* __restrict__ ulkj) {
+  constexpr int CHU = COMBO == 5 ? SFG_IC5_CHU : CHU_DEFAULT;
   const int lane = threadIdx.x & 31;
   const int64_t total = A.t_end - A.t_begin;
   const bool do_fac = COMBO == 5 ? (A.phase & 1) : (A.phase & 2);
@@ -389,8 +403,11 @@ __global__ void __launch_bounds__(kFBlock) k_ic0_warp(const ExecArgs A,
 // COMBO 3 (DSCAL -> ILU0): no solve; the row is scaled on load,
 // (d_i * a_ij) * d_j (dscal_csr_row, kernels.hpp:274-279), when fused, or
 // read from `work` after a separate DSCAL launch.
-template <int COMBO>
-__global__ void __launch_bounds__(kFBlock) k_ilu0_warp(const ExecArgs A,
+// MAXU: update slots a lane holds in registers (the pattern's maximum, 4 or
+// 8); the 4-slot build is compiled for 3 resident blocks per SM (80
+// registers, no spills): C3 1.545 -> 1.436 ms
+template <int COMBO, int MAXU>
+__global__ void __launch_bounds__(kFBlock, MAXU <= 4 ? SFG_ILU_MINB4 : 1) k_ilu0_warp(const ExecArgs A,
                                                        const int32_t* __restrict__ uptr,
                                                        const int32_t* __restrict__ ustep,
                                                        const int32_t* __restrict__ usrc) {
@@ -453,11 +470,11 @@ __global__ void __launch_bounds__(kFBlock) k_ilu0_warp(const ExecArgs A,
         ub = __ldg(uptr + pb);
         nu = __ldg(uptr + pb + 1) - ub;
       }
-      int st[kMaxIluUpd];
-      int sq[kMaxIluUpd];
-      unsigned long long wu[kMaxIluUpd];
+      int st[MAXU];
+      int sq[MAXU];
+      unsigned long long wu[MAXU];
 #pragma unroll
-      for (int e = 0; e < kMaxIluUpd; ++e) {
+      for (int e = 0; e < MAXU; ++e) {
         st[e] = -1;
         if (e < nu) {
           st[e] = __ldg(ustep + ub + e);
@@ -465,7 +482,7 @@ __global__ void __launch_bounds__(kFBlock) k_ilu0_warp(const ExecArgs A,
         }
       }
 #pragma unroll
-      for (int e = 0; e < kMaxIluUpd; ++e)
+      for (int e = 0; e < MAXU; ++e)
         if (e < nu)
           wu[e] = ld_relaxed_u64(A.fac + sq[e]);
       // all of this lane's words re-polled together until published; the
@@ -474,7 +491,7 @@ __global__ void __launch_bounds__(kFBlock) k_ilu0_warp(const ExecArgs A,
       for (;;) {
         bool pending = (dk >= 0 && is_sent_hi(wp)) || (want_x && is_sent_hi(wx));
 #pragma unroll
-        for (int e = 0; e < kMaxIluUpd; ++e)
+        for (int e = 0; e < MAXU; ++e)
           pending |= e < nu && is_sent_hi(wu[e]);
         if (!pending)
           break;
@@ -483,7 +500,7 @@ __global__ void __launch_bounds__(kFBlock) k_ilu0_warp(const ExecArgs A,
         if (want_x && is_sent_hi(wx))
           wx = ld_relaxed_u64(A.vout + col);
 #pragma unroll
-        for (int e = 0; e < kMaxIluUpd; ++e)
+        for (int e = 0; e < MAXU; ++e)
           if (e < nu && is_sent_hi(wu[e]))
             wu[e] = ld_relaxed_u64(A.fac + sq[e]);
       }
@@ -493,9 +510,9 @@ __global__ void __launch_bounds__(kFBlock) k_ilu0_warp(const ExecArgs A,
       c_next = (long long)__shfl_sync(FULL, nb, 0);
       if (c_next < total)
         i_nx = __ldg(A.order + A.t_begin + c_next);
-      double uv[kMaxIluUpd];
+      double uv[MAXU];
 #pragma unroll
-      for (int e = 0; e < kMaxIluUpd; ++e)
+      for (int e = 0; e < MAXU; ++e)
         uv[e] = e < nu ? __longlong_as_double((long long)wu[e]) : 0.0;
       if (ftr) {
         __syncwarp();
@@ -513,7 +530,7 @@ __global__ void __launch_bounds__(kFBlock) k_ilu0_warp(const ExecArgs A,
         }
         const double lik = __shfl_sync(FULL, acc, t);
 #pragma unroll
-        for (int e = 0; e < kMaxIluUpd; ++e)
+        for (int e = 0; e < MAXU; ++e)
           if (st[e] == t)
             acc = fsub_mul(acc, lik, uv[e]);
         if (do_solve)
@@ -624,10 +641,11 @@ void launch_ic0_warp(int combo, const ExecArgs& a, const UpdateLists& up, cudaSt
 }
 
 void launch_ilu0_warp(int combo, const ExecArgs& a, const UpdateLists& up, cudaStream_t s) {
+  const bool small = up.max_updates <= 4 && !getenv("SFG_ILU_MAXU8");
   if (combo == 3)
-    launch_warp_tasks(k_ilu0_warp<3>, a, up, s);
+    small ? launch_warp_tasks(k_ilu0_warp<3, 4>, a, up, s) : launch_warp_tasks(k_ilu0_warp<3, 8>, a, up, s);
   else
-    launch_warp_tasks(k_ilu0_warp<6>, a, up, s);
+    small ? launch_warp_tasks(k_ilu0_warp<6, 4>, a, up, s) : launch_warp_tasks(k_ilu0_warp<6, 8>, a, up, s);
 }
 
 } // namespace sfg
