@@ -17,6 +17,12 @@
 // instead of eight (116 registers, 2 blocks): C2 0.478 -> 0.444 ms
 #define SFG_IC5_CHU 4
 #endif
+#ifndef SFG_IC7_CHU
+#define SFG_IC7_CHU 4 // IC0 combo 7: update slots per batch (8: 9.53 ms, 4: 9.18 ms on C4)
+#endif
+#ifndef SFG_IC7_MINB
+#define SFG_IC7_MINB 1 // blocks per SM k_ic0_warp<7> is compiled for (A/B builds)
+#endif
 #ifndef SFG_IC5_MINB
 #define SFG_IC5_MINB 1 // blocks per SM k_ic0_warp<5> is compiled for (A/B builds)
 #endif
@@ -186,11 +192,11 @@ void build_lists(int32_t n, int64_t nnz, const int32_t* tptr, UpdateLists& out, 
 // applied on load (dscal_csc_col, kernels.hpp:281-286) for combo 7.
 //   src 0: column k from lc_val; 1: scaled on load; 2: pre-scaled in work.
 template <int COMBO>
-__global__ void __launch_bounds__(kFBlock, COMBO == 5 ? SFG_IC5_MINB : 1) k_ic0_warp(const ExecArgs A,
+__global__ void __launch_bounds__(kFBlock, COMBO == 5 ? SFG_IC5_MINB : SFG_IC7_MINB) k_ic0_warp(const ExecArgs A,
                                                       const int32_t* __restrict__ uptr,
                                                       const int32_t* __restrict__ usrc,
                                                       const int32_t* __restrict__ ulkj) {
-  constexpr int CHU = COMBO == 5 ? SFG_IC5_CHU : CHU_DEFAULT;
+  constexpr int CHU = COMBO == 5 ? SFG_IC5_CHU : SFG_IC7_CHU;
   const int lane = threadIdx.x & 31;
   const int64_t total = A.t_end - A.t_begin;
   const bool do_fac = COMBO == 5 ? (A.phase & 1) : (A.phase & 2);
