@@ -36,7 +36,6 @@ namespace sfg {
 namespace {
 
 constexpr int kFBlock = 256;
-constexpr int CHU_DEFAULT = 8; // IC0: updates staged per lane per batch
 constexpr int kMaxIluUpd = 8;  // ILU0: updates a lane holds in registers
 constexpr unsigned FULL = 0xffffffffu;
 
