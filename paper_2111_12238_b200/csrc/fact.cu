@@ -379,8 +379,12 @@ __global__ void __launch_bounds__(kFBlock, COMBO == 5 ? SFG_IC5_MINB : SFG_IC7_M
           xv = __longlong_as_double((long long)wx);
         }
         const int cnt = min(32, q1 - qb);
+        // each lane rounds its own product; the serial chain only shuffles
+        // and subtracts (the same separately rounded product and difference
+        // as fsub_mul, so the order and result are the reference's)
+        const double pr = __dmul_rn(lv, xv);
         for (int t = 0; t < cnt; ++t)
-          acc2 = fsub_mul(acc2, __shfl_sync(FULL, lv, t), __shfl_sync(FULL, xv, t));
+          acc2 = __dsub_rn(acc2, __shfl_sync(FULL, pr, t));
       }
       if (lane == 0) {
         if (lkk == 0.0)
@@ -558,8 +562,9 @@ __global__ void __launch_bounds__(kFBlock, MAXU <= 4 ? SFG_ILU_MINB4 : 1) k_ilu0
         lv = poll_f64(A.fac + pb, cap);
         xk = resolve(wx, A.vout + col, cap);
       }
+      const double pr = __dmul_rn(lv, xk); // per-lane product, as in k_ic0_warp
       for (int t = 0; t < nl; ++t)
-        acc2 = fsub_mul(acc2, __shfl_sync(FULL, lv, t), __shfl_sync(FULL, xk, t));
+        acc2 = __dsub_rn(acc2, __shfl_sync(FULL, pr, t));
     }
     if (do_solve && lane == 0) {
       publish_f64(A.vout + i, acc2);
