@@ -12,6 +12,16 @@
 #include "common.cuh"
 #include "fact.cuh"
 
+#ifndef SFG_IC_BUNROLL
+#define SFG_IC_BUNROLL 0 // unroll factor of the IC0 update-batch loop (2: C4 9.19 -> 9.63 ms)
+#endif
+#ifndef SFG_IC_UNROLL
+#define SFG_IC_UNROLL 2 // unroll factor of the IC0 solve-row loop (C2 0.368 -> 0.362 ms)
+#endif
+#ifndef SFG_ILU_UNROLL
+#define SFG_ILU_UNROLL 2 // unroll factor of the ILU0 pivot-step loop (C3 1.438 -> 1.123 ms; 3: 1.159, 4: 1.438)
+#endif
+
 #ifndef SFG_IC5_CHU
 // IC0 combo 5: update slots per batch.  Four (72 registers, 3 blocks per SM)
 // instead of eight (116 registers, 2 blocks): C2 0.478 -> 0.444 ms
@@ -263,6 +273,10 @@ __global__ void __launch_bounds__(kFBlock, COMBO == 5 ? SFG_IC5_MINB : SFG_IC7_M
         u0 = __ldg(uptr + pa);
         u1 = __ldg(uptr + pa + 1);
       }
+#if SFG_IC_BUNROLL
+      constexpr int kUnrollB = SFG_IC_BUNROLL;
+#pragma unroll kUnrollB
+#endif
       for (int u = u0; u < u1; u += CHU) {
         const int cnt = min(CHU, u1 - u);
         int ps[CHU], pl[CHU];
@@ -383,6 +397,10 @@ __global__ void __launch_bounds__(kFBlock, COMBO == 5 ? SFG_IC5_MINB : SFG_IC7_M
         // and subtracts (the same separately rounded product and difference
         // as fsub_mul, so the order and result are the reference's)
         const double pr = __dmul_rn(lv, xv);
+#if SFG_IC_UNROLL
+        constexpr int kUnrollS = SFG_IC_UNROLL;
+#pragma unroll kUnrollS
+#endif
         for (int t = 0; t < cnt; ++t)
           acc2 = __dsub_rn(acc2, __shfl_sync(FULL, pr, t));
       }
@@ -531,6 +549,10 @@ __global__ void __launch_bounds__(kFBlock, MAXU <= 4 ? SFG_ILU_MINB4 : 1) k_ilu0
       const double piv = dk >= 0 ? __longlong_as_double((long long)wp) : 0.0;
       const double rcp = __drcp_rn(piv);
       const double xk = want_x ? __longlong_as_double((long long)wx) : 0.0;
+#if SFG_ILU_UNROLL
+      constexpr int kUnroll = SFG_ILU_UNROLL;
+#pragma unroll kUnroll
+#endif
       for (int t = 0; t < nl; ++t) {
         if (lane == t) {
           if (dk < 0 || piv == 0.0)
