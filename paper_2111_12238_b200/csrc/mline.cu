@@ -1,5 +1,8 @@
 // mline.cu -- inspector and executor of the multi-chain warp scheme (see
 // mline.cuh).
+#ifndef SFG_ML1_UNROLL
+#define SFG_ML1_UNROLL 4 // unroll factor of k_mline1's step loop (C1 0.618 -> 0.587 ms; 2: 0.596)
+#endif
 #include "common.cuh"
 #include "mline.cuh"
 
@@ -649,7 +652,12 @@ __global__ void __launch_bounds__(kMThreads) k_mline1(const MLineArgs A) {
     if (A.trace)
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tr_claim));
     __syncwarp();
+#if SFG_ML1_UNROLL
+    constexpr int kUnrollM = SFG_ML1_UNROLL;
+#pragma unroll kUnrollM
+#else
 #pragma unroll 1
+#endif
     for (int i = -kRA1; i < T; ++i) {
       if (A.trace && i == 0)
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tr_first));
