@@ -585,6 +585,10 @@ __global__ void __launch_bounds__(kFBlock, MAXU <= 4 ? SFG_ILU_MINB4 : 1) k_ilu0
         xk = resolve(wx, A.vout + col, cap);
       }
       const double pr = __dmul_rn(lv, xk); // per-lane product, as in k_ic0_warp
+#if SFG_IC_UNROLL
+      constexpr int kUnrollU = SFG_IC_UNROLL;
+#pragma unroll kUnrollU
+#endif
       for (int t = 0; t < nl; ++t)
         acc2 = __dsub_rn(acc2, __shfl_sync(FULL, pr, t));
     }
