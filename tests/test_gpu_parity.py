@@ -631,3 +631,25 @@ def test_plans_concurrent_on_streams(orc):
     for st in plans:
         st.set_stream(None)
         st.close()
+
+
+# new values for every system of a batched plan (same pattern): the staged
+# chain executor re-reads them, fused and unfused, bit-exact
+@pytest.mark.parametrize("combo", (1, 8))
+def test_set_values_batched(orc, combo):
+    nsys = 4
+    M, vals = sf.config5_systems(size=12, nsys=nsys)
+    vin = np.concatenate([sf.gen_vector(M.n, 7 + s) for s in range(nsys)])
+    st = sf.make_state(combo, M, nsys=nsys, values=vals, vin=vin).inspect()
+    st.execute_fused()
+    rng = np.random.default_rng(combo)
+    v2 = vals * (1.0 + 0.05 * rng.uniform(0, 1, vals.size))
+    st.set_values(v2)
+    for run in (st.execute_fused, st.execute_unfused):
+        run()
+        got = st.collect_outputs().reshape(nsys, -1)
+        for s in range(nsys):
+            Ms = Csc(M.n, M.colptr, M.rowidx, v2[s * M.nnz:(s + 1) * M.nnz])
+            want = orc.run_sequential(combo, Ms, 7, vin=vin[s * M.n:(s + 1) * M.n])
+            assert np.array_equal(got[s], want), (combo, s, run.__name__)
+    st.close()
