@@ -19,6 +19,7 @@
 #include <cstring>
 #include <memory>
 #include <random>
+#include <cmath>
 #include <string>
 #include <vector>
 
@@ -593,6 +594,20 @@ ExecArgs exec_args(sfg_plan* P) {
     a.sleep_cap = 0;
   if (const char* e = getenv("SFG_SLEEP_CAP"))
     a.sleep_cap = (unsigned)atoi(e);
+  if (P->use_warpfac) {
+    // resident warps for about `look` levels of claimed tasks and no more:
+    // on a DAG of narrow levels the extra warps only spin beside the ones
+    // on the critical path (C4, ~110 columns per level: 4 -> 2 blocks/SM,
+    // 9.19 -> 8.70 ms); wide-level DAGs (C2, C3) keep full occupancy
+    int look = 20;
+    if (const char* e = getenv("SFG_FACT_LOOKAHEAD"))
+      look = atoi(e);
+    const int64_t waves = std::max<int64_t>(1, (int64_t)P->wave_ptr.size() - 1);
+    const double per_level = (double)P->n / (double)waves;
+    const double warps = look * per_level;
+    if (look > 0)
+      a.blocks_per_sm = std::max(1, (int)std::ceil(warps / (8.0 * sm_count())));
+  }
   if (const char* e = getenv("SFG_BLOCKS_PER_SM"))
     a.blocks_per_sm = atoi(e);
   if (P->use_warpfac && P->trace.p)
