@@ -55,8 +55,10 @@ template <typename T> struct DBuf {
   void alloc(int64_t count) {
     release();
     n = count;
+    // 64 bytes of tail slack: bulk copies round their source range out to
+    // 16-byte boundaries (chaintma.cu)
     if (count > 0)
-      SFG_CUDA(cudaMalloc(&p, sizeof(T) * (size_t)count));
+      SFG_CUDA(cudaMalloc(&p, sizeof(T) * (size_t)count + 64));
   }
   void release() {
     if (p)
