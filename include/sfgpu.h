@@ -124,6 +124,13 @@ sfg_status sfg_get_interdep(sfg_plan* plan, int32_t* nrows, int32_t* ncols,
 sfg_status sfg_get_levels(sfg_plan* plan, int32_t which, int32_t* level,
                           int32_t* height, int32_t* slack,
                           int32_t* critical_path);
+/* level_info (dag.hpp:197-218) of any DAG given by its successor CSR
+ * (edges must ascend; SFG_ERR_INVALID_ARGUMENT otherwise, the reference's
+ * "dependence cycle: edge does not ascend"), computed on the GPU without a
+ * plan.  Output arrays may be null. */
+sfg_status sfg_dag_levels(int32_t nvert, const int32_t* succptr, const int32_t* succ,
+                          int32_t* level, int32_t* height, int32_t* slack,
+                          int32_t* critical_path);
 /* compute_reuse (dag.hpp:398-431). */
 sfg_status sfg_compute_reuse(sfg_plan* plan, double* reuse);
 /* The fused schedule built by sfg_inspect: tickets in execution order as
@@ -149,6 +156,29 @@ sfg_status sfg_get_partitioning(sfg_plan* plan, int32_t* nspart, int64_t* nwpart
 sfg_status sfg_execute_fused(sfg_plan* plan);
 /* Unfused comparator: kernel 1 in one launch, kernel 2 in a second launch. */
 sfg_status sfg_execute_unfused(sfg_plan* plan);
+/* Joint-DAG wavefront executor (replaces execute_joint_wavefront,
+ * executor.hpp:465-507): the level sets of the joint DAG run one after
+ * another with a grid-wide barrier between them, each level's kernel-1 and
+ * kernel-2 iterations spread over every thread -- the paper's level-set
+ * baseline.  Same outputs as sfg_execute_fused (combo 4's CSC SpMV scatter
+ * accumulates with atomic adds, in any order, as the reference's does). */
+sfg_status sfg_execute_wavefront(sfg_plan* plan);
+/* execute_sequential (executor.hpp:315-322): run_sequential_reference --
+ * every kernel-1 iteration ascending, then every kernel-2 iteration -- on a
+ * single GPU thread.  The sequential baseline; same outputs. */
+sfg_status sfg_execute_sequential(sfg_plan* plan);
+/* Checks a flattened schedule (nentries (tag, iteration) pairs in execution
+ * order) against the plan's joint DAG on the GPU: *violations counts
+ * iterations missing or repeated plus joint-DAG edges u -> v with v placed
+ * before u; 0 means every sequential run of the entries computes what
+ * run_sequential_reference computes. */
+sfg_status sfg_check_schedule(sfg_plan* plan, int64_t nentries, const uint8_t* tags,
+                              const int32_t* iters, int64_t* violations);
+/* The level sets it runs (build_wavefront_schedule, executor.hpp:209-229):
+ * 2n entries (tag 1/2, iteration), ascending joint vertex id within a level,
+ * level_ptr[nlevels + 1].  Two-phase: call with null arrays for the sizes. */
+sfg_status sfg_get_wavefront(sfg_plan* plan, int64_t* nentries, uint8_t* tags,
+                             int32_t* iters, int32_t* nlevels, int64_t* level_ptr);
 /* nsteps executions with new input vectors -- equivalent to nsteps rounds of
  * sfg_set_vin + sfg_execute_fused + sfg_collect_outputs -- with the
  * transfers overlapped with compute: step k+1's input is copied in and step
@@ -185,6 +215,10 @@ sfg_status sfg_spmv_rows(sfg_plan* plan, int32_t r0, int32_t r1, const double* x
                          double* y_device);
 /* Waits for the plan stream; returns SFG_ERR_FACTORIZATION on breakdown. */
 sfg_status sfg_synchronize(sfg_plan* plan);
+/* reset (kernels.hpp:498-502): fac = the factor's input values, vmid = vout
+ * = 0, so collect_outputs and sfg_execute_kernel(2) see what the reference's
+ * reset leaves.  (Every sfg_execute_* call re-initialises its own outputs.) */
+sfg_status sfg_reset(sfg_plan* plan);
 /* collect_outputs (kernels.hpp:585-608) for every system, system-major,
  * into host memory; synchronizes.  cap in doubles. */
 sfg_status sfg_collect_outputs(sfg_plan* plan, double* out_host, int64_t cap);
@@ -207,8 +241,9 @@ sfg_status sfg_last_exec_ms(sfg_plan* plan, float* total_ms, float* kernel_ms);
 /* Back-to-back executions on the plan stream, timed with CUDA events
  * recorded on that stream: total_ms covers all `reps` executions (output
  * re-initialisation included); kernel_ms_avg is the mean duration of the
- * main executor kernel per execution.  unfused != 0 times the two-launch
- * comparator instead.  Returns SFG_ERR_FACTORIZATION on breakdown. */
+ * main executor kernel per execution.  unfused = 1 times the two-launch
+ * comparator instead, unfused = 2 the joint-DAG wavefront executor.
+ * Returns SFG_ERR_FACTORIZATION on breakdown. */
 sfg_status sfg_bench_executions(sfg_plan* plan, int32_t reps, int32_t unfused,
                                 float* total_ms, float* kernel_ms_avg);
 

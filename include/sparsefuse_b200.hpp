@@ -3,30 +3,48 @@
 // sfgpu.h.  Header-only; link with -lsfgpu (paper_2111_12238_b200/libsfgpu.so).
 //
 // A caller of the reference switches with
+//     #include "sparsefuse_b200.hpp"
 //     namespace sparsefuse = sparsefuse_b200;
-// and keeps its call sequence:
-//     auto st = make_state(combo, M, seed);          // kernels.hpp:429
-//     auto g1 = build_g1(st), g2 = build_g2(st);     // dag.hpp:319,339
-//     auto f  = inter_dag(st);                       // dag.hpp:279
+// and keeps its call sequence (proj/demos/fuse_demo.cpp:15-31,
+// proj/tools/sfuse.cpp:113-155):
+//     KernelState st = make_state(combo, M, seed);   // kernels.hpp:429
+//     DepDag g1 = build_g1(st), g2 = build_g2(st);   // dag.hpp:319,339
+//     InterDep f = inter_dag(st);                    // dag.hpp:279
 //     double reuse = compute_reuse(st);              // dag.hpp:398
-//     auto sched = make_fused_schedule(st);          // msp + compile_schedule
-//     execute_fused(sched, st);                      // executor.hpp:395
+//     FusedPartitioning V = msp(g1, g2, f, r, reuse);           // msp.hpp:825
+//     auto bad = validate_fused_partitioning(V, g1, g2, f);     // msp.hpp:1114
+//     FusedSchedule sched = compile_schedule(V, reuse, g1, g2, r); // executor.hpp:235
+//     execute_fused(sched, st, r);                   // executor.hpp:395
+//     execute_unfused(g1, g2, st, r);                // executor.hpp:383
+//     execute_joint_wavefront(g1, g2, f, st, r);     // executor.hpp:500
+//     execute_sequential(st);                        // executor.hpp:315
 //     auto out = collect_outputs(st);                // kernels.hpp:585
 // Differences, all deliberate:
 //  * KernelState owns device memory (move-only); its operands are not public
 //    std::vectors.  collect_outputs copies the results back.
-//  * The fused schedule is built on the GPU by the inspector (level order of
-//    the joint DAG, claimed by tickets) instead of msp (msp.hpp:825-1082); the
-//    r / redundancy / nthreads arguments have no GPU meaning and are accepted
-//    and ignored so call sites compile unchanged.
-//  * joint_dag / level_info take the state (the GPU builds them); the
-//    structures returned have the reference's layout and values bit for bit.
-//  * No CPU fallback: without a CUDA device make_state throws NoDeviceError.
+//  * msp returns the GPU inspector's partitioning of the state the DAGs came
+//    from (they carry its identity): s-partitions = dependency levels of the
+//    executor's work units, checked by validate_fused_partitioning like any
+//    MSP output.  For DAGs built elsewhere it returns the joint DAG's level
+//    sets split into r w-partitions.  r / redundancy / nthreads have no GPU
+//    meaning beyond that.
+//  * execute_fused checks the schedule it is handed against the state's
+//    joint DAG on the GPU (every iteration once, every dependence ordered)
+//    and throws std::invalid_argument if it is not a valid order; a valid
+//    schedule computes the same result as any other, so the state's own
+//    executor runs it.
+//  * No CPU fallback: without a CUDA device make_state throws NoDeviceError,
+//    and execute_sequential runs the reference's sequential loop on one GPU
+//    thread.
 #pragma once
 
+#include <algorithm>
+#include <array>
 #include <cstdint>
+#include <mutex>
 #include <stdexcept>
 #include <string>
+#include <unordered_map>
 #include <utility>
 #include <vector>
 
@@ -87,6 +105,9 @@ struct DepDag {
   std::vector<Index> succptr;
   std::vector<Index> succ;
   std::vector<Cost> cost;
+  // the KernelState this DAG was built from (0: built elsewhere); lets msp /
+  // joint_dag / the executors use that state's GPU inspector
+  std::uint64_t origin = 0;
   Index nedges() const { return succptr.empty() ? 0 : succptr.back(); }
   Cost total_cost() const {
     Cost t = 0;
@@ -102,6 +123,7 @@ struct InterDep {
   Index ncols = 0;
   std::vector<Index> rowptr;
   std::vector<Index> colidx;
+  std::uint64_t origin = 0; // as DepDag::origin
   Index nnz() const { return rowptr.empty() ? 0 : rowptr.back(); }
 };
 
@@ -116,7 +138,8 @@ struct LevelInfo {
 // executor.hpp:84-90 (timings of one GPU execution; no per-thread busy times)
 struct ExecStats {
   std::int64_t wall_ns = 0;  // device time of the execution (CUDA events)
-  Index barriers = 0;        // always 0: the executor has no barriers
+  Index barriers = 0;        // 0 for the barrier-free executors; levels - 1 for the wavefront
+  std::vector<std::vector<std::int64_t>> busy_ns; // (no per-thread busy times on the GPU)
   std::int64_t launches = 0; // kernels launched by the execution
 };
 
@@ -129,6 +152,25 @@ inline std::string last_message(const sfg_plan* p, std::int32_t* kind, std::int3
   if (p)
     sfg_last_error(p, kind, index, buf, (std::int32_t)sizeof(buf));
   return std::string(buf);
+}
+
+// live KernelStates by id, so DAGs can name the state they came from
+struct Registry {
+  std::mutex mu;
+  std::unordered_map<std::uint64_t, sfg_plan*> live;
+  std::uint64_t next = 1;
+};
+inline Registry& registry() {
+  static Registry r;
+  return r;
+}
+inline sfg_plan* plan_of(std::uint64_t id) {
+  if (!id)
+    return nullptr;
+  Registry& r = registry();
+  std::lock_guard<std::mutex> lk(r.mu);
+  auto it = r.live.find(id);
+  return it == r.live.end() ? nullptr : it->second;
 }
 
 inline void check(const sfg_plan* p, sfg_status st, const char* what) {
@@ -175,7 +217,9 @@ public:
       nnz_m_ = o.nnz_m_;
       output_len_ = o.output_len_;
       inspected_ = o.inspected_;
+      id_ = o.id_;
       o.plan_ = nullptr;
+      o.id_ = 0;
     }
     return *this;
   }
@@ -186,6 +230,7 @@ public:
   Index nsys() const { return nsys_; }
   std::int64_t output_len() const { return output_len_; } // per system
   sfg_plan* handle() const { return plan_; }
+  std::uint64_t id() const { return id_; }
 
   // st.vin = ... (kernels.hpp:420): nsys*n doubles, system-major
   void set_vin(const std::vector<double>& vin) {
@@ -210,11 +255,18 @@ private:
   friend KernelState make_state(int, const CscMatrix&, std::uint64_t, Index,
                                 const std::vector<double>*, const std::vector<double>*);
   void release() {
+    if (id_) {
+      detail::Registry& r = detail::registry();
+      std::lock_guard<std::mutex> lk(r.mu);
+      r.live.erase(id_);
+      id_ = 0;
+    }
     if (plan_)
       sfg_plan_destroy(plan_);
     plan_ = nullptr;
   }
   sfg_plan* plan_ = nullptr;
+  std::uint64_t id_ = 0;
   int combo_ = 0;
   Index nsys_ = 1;
   std::int64_t nnz_m_ = 0;
@@ -262,6 +314,12 @@ inline KernelState make_state(int combo_id, const CscMatrix& M, std::uint64_t se
   std::int64_t nnzf = 0, olen = 0;
   detail::check(p, sfg_plan_info(p, &c, &nn, &ns, &nnzf, &olen), "plan_info");
   st.output_len_ = olen;
+  {
+    detail::Registry& r = detail::registry();
+    std::lock_guard<std::mutex> lk(r.mu);
+    st.id_ = r.next++;
+    r.live[st.id_] = p;
+  }
   return st;
 }
 
@@ -279,6 +337,7 @@ inline DepDag get_dag(KernelState& st, std::int32_t which) {
         sfg_get_dag(st.handle(), which, &g.nvert, &ne, g.succptr.data(), g.succ.data(),
                     g.cost.data()),
         "get_dag");
+  g.origin = st.id();
   return g;
 }
 } // namespace detail
@@ -303,6 +362,7 @@ inline InterDep inter_dag(KernelState& st) {
                 sfg_get_interdep(st.handle(), &f.nrows, &f.ncols, &nnz, f.rowptr.data(),
                                  f.colidx.data()),
                 "inter_dag");
+  f.origin = st.id();
   return f;
 }
 
@@ -321,6 +381,67 @@ inline LevelInfo level_info(KernelState& st, int which) {
   return li;
 }
 
+// level_info(const DepDag&) (dag.hpp:197-218) of any DAG, on the GPU.  An
+// edge that does not ascend throws std::invalid_argument like the reference.
+inline LevelInfo level_info(const DepDag& g) {
+  LevelInfo li;
+  li.level.resize((size_t)g.nvert);
+  li.height.resize((size_t)g.nvert);
+  li.slack.resize((size_t)g.nvert);
+  const sfg_status s = sfg_dag_levels(g.nvert, g.succptr.data(), g.succ.data(), li.level.data(),
+                                      li.height.data(), li.slack.data(), &li.critical_path);
+  if (s == SFG_ERR_INVALID_ARGUMENT)
+    throw std::invalid_argument("dependence cycle: edge does not ascend");
+  detail::check(nullptr, s, "level_info");
+  return li;
+}
+
+// joint_dag (dag.hpp:222-238): G1, G2 offset by |V1|, and (j, |V1| + i) for
+// every F_ij.  DAGs of one live state come from its GPU inspector; others
+// are merged here (sorted, duplicate-free successor lists, costs concatenated).
+inline DepDag joint_dag(const DepDag& g1, const DepDag& g2, const InterDep& f) {
+  if (g1.origin && g1.origin == g2.origin && g1.origin == f.origin) {
+    if (sfg_plan* p = detail::plan_of(g1.origin)) {
+      DepDag j;
+      std::int64_t ne = 0;
+      detail::check(p, sfg_get_dag(p, 3, &j.nvert, &ne, nullptr, nullptr, nullptr), "joint_dag");
+      j.succptr.resize((size_t)j.nvert + 1);
+      j.succ.resize((size_t)ne);
+      j.cost.resize((size_t)j.nvert);
+      detail::check(p, sfg_get_dag(p, 3, &j.nvert, &ne, j.succptr.data(), j.succ.data(),
+                                   j.cost.data()),
+                    "joint_dag");
+      j.origin = g1.origin;
+      return j;
+    }
+  }
+  const Index n1 = g1.nvert, nv = g1.nvert + g2.nvert;
+  std::vector<std::vector<Index>> adj((size_t)nv);
+  for (Index u = 0; u < n1; ++u)
+    for (Index p = g1.succptr[(size_t)u]; p < g1.succptr[(size_t)u + 1]; ++p)
+      adj[(size_t)u].push_back(g1.succ[(size_t)p]);
+  for (Index u = 0; u < g2.nvert; ++u)
+    for (Index p = g2.succptr[(size_t)u]; p < g2.succptr[(size_t)u + 1]; ++p)
+      adj[(size_t)(n1 + u)].push_back(n1 + g2.succ[(size_t)p]);
+  for (Index i = 0; i < f.nrows; ++i)
+    for (Index p = f.rowptr[(size_t)i]; p < f.rowptr[(size_t)i + 1]; ++p)
+      adj[(size_t)f.colidx[(size_t)p]].push_back(n1 + i);
+  DepDag j;
+  j.nvert = nv;
+  j.succptr.assign((size_t)nv + 1, 0);
+  for (Index u = 0; u < nv; ++u) {
+    auto& a = adj[(size_t)u];
+    std::sort(a.begin(), a.end());
+    a.erase(std::unique(a.begin(), a.end()), a.end());
+    j.succptr[(size_t)u + 1] = j.succptr[(size_t)u] + (Index)a.size();
+  }
+  for (auto& a : adj)
+    j.succ.insert(j.succ.end(), a.begin(), a.end());
+  j.cost = g1.cost;
+  j.cost.insert(j.cost.end(), g2.cost.begin(), g2.cost.end());
+  return j;
+}
+
 // dag.hpp:398-431
 inline double compute_reuse(KernelState& st) {
   double r = 0.0;
@@ -328,42 +449,8 @@ inline double compute_reuse(KernelState& st) {
   return r;
 }
 
-// FusedSchedule (executor.hpp:138-150): the GPU inspector's ticket order --
-// every (tag, iter) of both kernels in a linear extension of the joint DAG,
-// grouped into wavefronts.  `interleaved` follows compile_schedule's rule
-// (reuse >= 1, executor.hpp:240).
-struct FusedSchedule {
-  bool fusion = true;
-  bool interleaved = false;
-  std::vector<std::uint8_t> tags; // 1 = kernel-1 iteration, 2 = kernel-2
-  std::vector<Index> iters;
-  std::vector<std::int64_t> wave_ptr;
-  Index nspartitions() const { return wave_ptr.empty() ? 0 : (Index)wave_ptr.size() - 1; }
-};
-
-// msp (msp.hpp:825-1082) + compile_schedule (executor.hpp:235-268)
-inline FusedSchedule make_fused_schedule(KernelState& st, Index /*r*/ = 0,
-                                         double /*redundancy*/ = 2.0) {
-  st.inspect();
-  FusedSchedule fs;
-  std::int64_t ne = 0;
-  std::int32_t nw = 0;
-  detail::check(st.handle(),
-                sfg_get_schedule(st.handle(), &ne, nullptr, nullptr, &nw, nullptr), "schedule");
-  fs.tags.resize((size_t)ne);
-  fs.iters.resize((size_t)ne);
-  fs.wave_ptr.resize((size_t)nw + 1);
-  detail::check(st.handle(),
-                sfg_get_schedule(st.handle(), &ne, fs.tags.data(), fs.iters.data(), &nw,
-                                 fs.wave_ptr.data()),
-                "schedule");
-  fs.interleaved = compute_reuse(st) >= 1.0;
-  return fs;
-}
-
-// FusedEntry / FusedPartitioning (msp.hpp:19-63): the same schedule as nested
-// s-partitions (run in order) of independent w-partitions (ordered entries),
-// checkable with the reference's validate_fused_partitioning.
+// FusedEntry / FusedPartitioning (msp.hpp:19-63): nested s-partitions (run in
+// order) of independent w-partitions (ordered entries).
 struct FusedEntry {
   std::uint8_t tag = 1;
   Index iter = 0;
@@ -375,28 +462,52 @@ struct FusedPartitioning {
   double reuse_ratio = 0.0;
   Index n1 = 0, n2 = 0;
   std::vector<std::vector<std::vector<FusedEntry>>> spartitions;
+  std::vector<std::array<Index, 4>> pairs; // (s, w) of paired partitions (none from the GPU)
+  std::uint64_t origin = 0;                // state whose inspector built it (0: none)
   Index b() const { return static_cast<Index>(spartitions.size()); }
 };
 
-inline FusedPartitioning fused_partitioning(KernelState& st) {
-  st.inspect();
+// FusedSchedule (executor.hpp:138-150): flattened partitioning.
+struct FusedSchedule {
+  bool fusion = true;
+  bool interleaved = false;
+  struct WRange {
+    Index begin, end, split;
+    Cost cost;
+  };
+  std::vector<FusedEntry> entries;
+  std::vector<std::vector<WRange>> sparts;
+  std::uint64_t checked_for = 0; // state the entries were verified against
+  Index nspartitions() const { return static_cast<Index>(sparts.size()); }
+};
+
+// WavefrontSchedule (executor.hpp:152-156): joint-DAG level sets.
+struct WavefrontSchedule {
+  std::vector<FusedEntry> entries;
+  std::vector<std::pair<Index, Index>> levels; // [begin, end) per level
+};
+
+namespace detail {
+// The GPU inspector's partitioning of a state (sfg_get_partitioning).
+inline FusedPartitioning gpu_partitioning(sfg_plan* p, std::uint64_t id, Index n) {
+  detail::check(p, sfg_inspect(p), "inspect");
   std::int32_t ns = 0;
   std::int64_t nw = 0, ne = 0;
-  detail::check(st.handle(),
-                sfg_get_partitioning(st.handle(), &ns, &nw, &ne, nullptr, nullptr, nullptr,
-                                     nullptr),
-                "partitioning");
+  check(p, sfg_get_partitioning(p, &ns, &nw, &ne, nullptr, nullptr, nullptr, nullptr),
+        "partitioning");
   std::vector<std::int64_t> sp((size_t)ns + 1), wp((size_t)nw + 1);
   std::vector<std::uint8_t> tg((size_t)ne);
   std::vector<Index> it((size_t)ne);
-  detail::check(st.handle(),
-                sfg_get_partitioning(st.handle(), nullptr, nullptr, nullptr, sp.data(),
-                                     wp.data(), tg.data(), it.data()),
-                "partitioning");
+  check(p, sfg_get_partitioning(p, nullptr, nullptr, nullptr, sp.data(), wp.data(), tg.data(),
+                                it.data()),
+        "partitioning");
   FusedPartitioning V;
-  V.reuse_ratio = compute_reuse(st);
-  V.interleaved = V.reuse_ratio >= 1.0;
-  V.n1 = V.n2 = st.n;
+  double r = 0.0;
+  check(p, sfg_compute_reuse(p, &r), "compute_reuse");
+  V.reuse_ratio = r;
+  V.interleaved = r >= 1.0;
+  V.n1 = V.n2 = n;
+  V.origin = id;
   V.spartitions.resize((size_t)ns);
   for (std::int32_t k = 0; k < ns; ++k)
     for (std::int64_t w = sp[(size_t)k]; w < sp[(size_t)k + 1]; ++w) {
@@ -406,6 +517,234 @@ inline FusedPartitioning fused_partitioning(KernelState& st) {
       V.spartitions[(size_t)k].push_back(std::move(es));
     }
   return V;
+}
+
+inline void flatten(const FusedSchedule& s, std::vector<std::uint8_t>& tags,
+                    std::vector<Index>& iters) {
+  tags.resize(s.entries.size());
+  iters.resize(s.entries.size());
+  for (size_t q = 0; q < s.entries.size(); ++q) {
+    tags[q] = s.entries[q].tag;
+    iters[q] = s.entries[q].iter;
+  }
+}
+
+// violations of a flattened order against a state's joint DAG (GPU)
+inline std::int64_t order_violations(sfg_plan* p, const FusedSchedule& s) {
+  std::vector<std::uint8_t> tags;
+  std::vector<Index> iters;
+  flatten(s, tags, iters);
+  std::int64_t bad = 0;
+  check(p, sfg_check_schedule(p, (std::int64_t)tags.size(), tags.data(), iters.data(), &bad),
+        "check_schedule");
+  return bad;
+}
+} // namespace detail
+
+// The state's GPU inspector partitioning (sfg_get_partitioning).
+inline FusedPartitioning fused_partitioning(KernelState& st) {
+  st.inspect();
+  return detail::gpu_partitioning(st.handle(), st.id(), st.n);
+}
+
+// msp (msp.hpp:825-1082).  For DAGs of a live state: that state's GPU
+// inspector partitioning (what execute_fused runs).  Otherwise: the joint
+// DAG's level sets (computed on the GPU), each split into at most r
+// contiguous w-partitions -- a valid fused partitioning of any DAG pair.
+// Packing follows reuse_ratio (interleaved iff >= 1, msp.hpp:834).
+inline FusedPartitioning msp(const DepDag& g1, const DepDag& g2, const InterDep& f, Index r,
+                             double reuse_ratio, double /*redundancy_factor*/ = 2.0) {
+  if (r < 1)
+    throw std::invalid_argument("partition count must be >= 1");
+  FusedPartitioning V;
+  if (g1.origin && g1.origin == g2.origin && g1.origin == f.origin) {
+    if (sfg_plan* p = detail::plan_of(g1.origin)) {
+      V = detail::gpu_partitioning(p, g1.origin, g1.nvert);
+      V.reuse_ratio = reuse_ratio;
+      V.interleaved = reuse_ratio >= 1.0;
+      return V;
+    }
+  }
+  V.n1 = g1.nvert;
+  V.n2 = g2.nvert;
+  V.reuse_ratio = reuse_ratio;
+  V.interleaved = reuse_ratio >= 1.0;
+  const DepDag j = joint_dag(g1, g2, f);
+  const LevelInfo li = level_info(j);
+  std::vector<std::vector<Index>> lev((size_t)li.critical_path + 1);
+  for (Index v = 0; v < j.nvert; ++v)
+    lev[(size_t)li.level[(size_t)v]].push_back(v);
+  for (Index l = 1; l <= li.critical_path; ++l) {
+    const auto& vs = lev[(size_t)l];
+    const Index len = (Index)vs.size(), parts = std::min<Index>(r, len);
+    std::vector<std::vector<FusedEntry>> sp;
+    for (Index w = 0; w < parts; ++w) {
+      std::vector<FusedEntry> es;
+      for (Index q = w * len / parts; q < (w + 1) * len / parts; ++q) {
+        const Index v = vs[(size_t)q];
+        es.push_back(v < g1.nvert ? FusedEntry{1, v, false} : FusedEntry{2, v - g1.nvert, false});
+      }
+      sp.push_back(std::move(es));
+    }
+    V.spartitions.push_back(std::move(sp));
+  }
+  return V;
+}
+
+namespace detail {
+inline void invert(const DepDag& g, std::vector<Index>& pp, std::vector<Index>& pr) {
+  pp.assign((size_t)g.nvert + 1, 0);
+  for (Index e = 0; e < g.nedges(); ++e)
+    ++pp[(size_t)g.succ[(size_t)e] + 1];
+  for (Index v = 0; v < g.nvert; ++v)
+    pp[(size_t)v + 1] += pp[(size_t)v];
+  pr.assign((size_t)g.nedges(), 0);
+  std::vector<Index> cur(pp.begin(), pp.end() - 1);
+  for (Index u = 0; u < g.nvert; ++u)
+    for (Index p = g.succptr[(size_t)u]; p < g.succptr[(size_t)u + 1]; ++p)
+      pr[(size_t)cur[(size_t)g.succ[(size_t)p]]++] = u;
+}
+} // namespace detail
+
+// validate_fused_partitioning (msp.hpp:1110-1237): coverage, duplicate
+// provenance, within-partition linear extension and the cross-partition
+// ordering invariant, with the reference's messages; empty means valid.
+inline std::vector<std::string> validate_fused_partitioning(const FusedPartitioning& V,
+                                                            const DepDag& g1, const DepDag& g2,
+                                                            const InterDep& f) {
+  std::vector<std::string> bad;
+  if (!V.fusion) {
+    if (V.b() != 0)
+      bad.push_back("fusion disabled but schedule non-empty");
+    return bad;
+  }
+  auto complain = [&](Index s, Index w, Index e, const std::string& what) {
+    bad.push_back("(s=" + std::to_string(s) + ",w=" + std::to_string(w) +
+                  ",entry=" + std::to_string(e) + "): " + what);
+  };
+  struct Pos {
+    Index s, w, idx;
+  };
+  std::vector<std::vector<Pos>> pos1((size_t)g1.nvert);
+  std::vector<Pos> pos2((size_t)g2.nvert, Pos{-1, -1, -1});
+  std::vector<Index> count2((size_t)g2.nvert, 0);
+  for (Index s = 0; s < V.b(); ++s)
+    for (Index w = 0; w < (Index)V.spartitions[(size_t)s].size(); ++w) {
+      const auto& es = V.spartitions[(size_t)s][(size_t)w];
+      for (Index e = 0; e < (Index)es.size(); ++e) {
+        const FusedEntry& fe = es[(size_t)e];
+        if (fe.tag == 1) {
+          if (fe.iter < 0 || fe.iter >= g1.nvert)
+            complain(s, w, e, "kernel-1 iteration out of range");
+          else
+            pos1[(size_t)fe.iter].push_back({s, w, e});
+        } else if (fe.iter < 0 || fe.iter >= g2.nvert) {
+          complain(s, w, e, "kernel-2 iteration out of range");
+        } else {
+          if (++count2[(size_t)fe.iter] > 1)
+            complain(s, w, e, "kernel-2 iteration duplicated");
+          pos2[(size_t)fe.iter] = {s, w, e};
+        }
+      }
+    }
+  for (Index v = 0; v < g1.nvert; ++v)
+    if (pos1[(size_t)v].empty())
+      bad.push_back("kernel-1 iteration " + std::to_string(v) + " missing");
+  for (Index v = 0; v < g2.nvert; ++v)
+    if (count2[(size_t)v] == 0)
+      bad.push_back("kernel-2 iteration " + std::to_string(v) + " missing");
+  if (!bad.empty())
+    return bad;
+  for (Index v = 0; v < g1.nvert; ++v)
+    if (pos1[(size_t)v].size() > 1)
+      for (const Pos& p : pos1[(size_t)v])
+        if (!V.spartitions[(size_t)p.s][(size_t)p.w][(size_t)p.idx].dup)
+          complain(p.s, p.w, p.idx, "replicated entry not flagged dup");
+  std::vector<Index> p1, r1, p2, r2;
+  detail::invert(g1, p1, r1);
+  detail::invert(g2, p2, r2);
+  auto earliest1 = [&](Index u) {
+    Index s = V.b();
+    for (const Pos& p : pos1[(size_t)u])
+      s = std::min(s, p.s);
+    return s;
+  };
+  auto before = [&](const Pos& at, Index u, std::uint8_t tag) {
+    const auto& es = V.spartitions[(size_t)at.s][(size_t)at.w];
+    for (Index e = 0; e < at.idx; ++e)
+      if (es[(size_t)e].tag == tag && es[(size_t)e].iter == u)
+        return true;
+    return false;
+  };
+  for (Index v = 0; v < g1.nvert; ++v)
+    for (const Pos& pv : pos1[(size_t)v])
+      for (Index p = p1[(size_t)v]; p < p1[(size_t)v + 1]; ++p) {
+        const Index u = r1[(size_t)p];
+        if (!before(pv, u, 1) && earliest1(u) >= pv.s)
+          complain(pv.s, pv.w, pv.idx, "kernel-1 dependence on " + std::to_string(u) + " unsatisfied");
+      }
+  for (Index v = 0; v < g2.nvert; ++v) {
+    const Pos& pv = pos2[(size_t)v];
+    for (Index p = p2[(size_t)v]; p < p2[(size_t)v + 1]; ++p) {
+      const Index u = r2[(size_t)p];
+      const Pos& pu = pos2[(size_t)u];
+      if (!(pu.s < pv.s || (pu.s == pv.s && pu.w == pv.w && pu.idx < pv.idx)))
+        complain(pv.s, pv.w, pv.idx, "kernel-2 dependence on " + std::to_string(u) + " unsatisfied");
+    }
+    for (Index p = f.rowptr[(size_t)v]; p < f.rowptr[(size_t)v + 1]; ++p) {
+      const Index u = f.colidx[(size_t)p];
+      if (!before(pv, u, 1) && earliest1(u) >= pv.s)
+        complain(pv.s, pv.w, pv.idx,
+                 "cross-kernel dependence on " + std::to_string(u) + " unsatisfied");
+    }
+  }
+  return bad;
+}
+
+// compile_schedule (executor.hpp:235-268): flattens V; interleaved iff
+// reuse_ratio >= 1; separated ranges get their kernel-1 / kernel-2 split.
+// The entries are checked against the state the DAGs came from (if live).
+inline FusedSchedule compile_schedule(const FusedPartitioning& V, double reuse_ratio,
+                                      const DepDag& g1, const DepDag& g2, Index /*r*/) {
+  FusedSchedule fs;
+  fs.fusion = V.fusion;
+  fs.interleaved = reuse_ratio >= 1.0;
+  for (const auto& sp : V.spartitions) {
+    std::vector<FusedSchedule::WRange> ws;
+    for (const auto& wp : sp) {
+      const Index begin = (Index)fs.entries.size();
+      Cost c = 0;
+      for (const FusedEntry& e : wp) {
+        fs.entries.push_back(e);
+        const auto& cost = e.tag == 1 ? g1.cost : g2.cost;
+        if (e.iter >= 0 && (size_t)e.iter < cost.size())
+          c += cost[(size_t)e.iter];
+      }
+      Index split = (Index)fs.entries.size();
+      if (!fs.interleaved) {
+        split = begin;
+        while (split < (Index)fs.entries.size() && fs.entries[(size_t)split].tag == 1)
+          ++split;
+      }
+      ws.push_back({begin, (Index)fs.entries.size(), split, c});
+    }
+    fs.sparts.push_back(std::move(ws));
+  }
+  if (g1.origin && g1.origin == g2.origin)
+    if (sfg_plan* p = detail::plan_of(g1.origin))
+      if (detail::order_violations(p, fs) == 0)
+        fs.checked_for = g1.origin;
+  return fs;
+}
+
+// The state's own fused schedule (the GPU inspector's, compile_schedule'd).
+inline FusedSchedule make_fused_schedule(KernelState& st, Index r = 1, double /*redundancy*/ = 2.0) {
+  const FusedPartitioning V = fused_partitioning(st);
+  FusedSchedule fs;
+  DepDag g; // costs are not needed by the executor
+  fs = compile_schedule(V, V.reuse_ratio, g, g, r);
+  fs.checked_for = st.id();
+  return fs;
 }
 
 namespace detail {
@@ -418,14 +757,31 @@ inline ExecStats finish(KernelState& st, std::int64_t launches0) {
   es.launches = sfg_launch_count(st.handle()) - launches0;
   return es;
 }
+
+// DAGs passed to an executor must describe the state
+inline void same_state(const KernelState& st, const DepDag& g1, const DepDag& g2) {
+  if ((g1.origin && g1.origin != st.id()) || (g2.origin && g2.origin != st.id()) ||
+      g1.nvert != st.n || g2.nvert != st.n)
+    throw std::invalid_argument("the DAGs do not belong to this KernelState");
+}
 } // namespace detail
 
 // executor.hpp:395-461 -- one fused launch; resets the outputs first (reset,
 // kernels.hpp:498-502, is part of every execution).  Synchronous like the
-// reference; FactorizationError carries the failing index.
-inline ExecStats execute_fused(const FusedSchedule& /*sched*/, KernelState& st,
+// reference; FactorizationError carries the failing index.  A schedule not
+// verified for this state is checked on the GPU first (std::invalid_argument
+// if an iteration is missing/repeated or a dependence is out of order).
+inline ExecStats execute_fused(const FusedSchedule& sched, KernelState& st,
                                Index /*nthreads*/ = 0) {
   st.inspect();
+  if (!sched.fusion)
+    throw std::logic_error("execute_fused: fusion disabled, run the fallback schedule");
+  if (sched.checked_for != st.id()) {
+    const std::int64_t bad = detail::order_violations(st.handle(), sched);
+    if (bad)
+      throw std::invalid_argument("execute_fused: schedule violates the joint DAG of this state (" +
+                                  std::to_string(bad) + " violations)");
+  }
   const std::int64_t l0 = sfg_launch_count(st.handle());
   detail::check(st.handle(), sfg_execute_fused(st.handle()), "execute_fused");
   return detail::finish(st, l0);
@@ -436,8 +792,80 @@ inline ExecStats execute_unfused(KernelState& st, Index /*nthreads*/ = 0) {
   st.inspect();
   const std::int64_t l0 = sfg_launch_count(st.handle());
   detail::check(st.handle(), sfg_execute_unfused(st.handle()), "execute_unfused");
+  ExecStats es = detail::finish(st, l0);
+  es.barriers = 1;
+  return es;
+}
+// executor.hpp:383-392 (the reference builds the LBC schedules of g1 / g2)
+inline ExecStats execute_unfused(const DepDag& g1, const DepDag& g2, KernelState& st,
+                                 Index nthreads = 0) {
+  detail::same_state(st, g1, g2);
+  return execute_unfused(st, nthreads);
+}
+
+// build_wavefront_schedule (executor.hpp:209-229): the joint DAG's level
+// sets, ascending vertex id within a level (from the state's GPU inspector
+// when the DAGs come from a live state).
+inline WavefrontSchedule build_wavefront_schedule(const DepDag& g1, const DepDag& g2,
+                                                  const InterDep& f) {
+  WavefrontSchedule ws;
+  sfg_plan* p = (g1.origin && g1.origin == g2.origin && g1.origin == f.origin)
+                    ? detail::plan_of(g1.origin)
+                    : nullptr;
+  if (p) {
+    std::int64_t ne = 0;
+    std::int32_t nl = 0;
+    detail::check(p, sfg_get_wavefront(p, &ne, nullptr, nullptr, &nl, nullptr), "wavefront");
+    std::vector<std::uint8_t> tg((size_t)ne);
+    std::vector<Index> it((size_t)ne);
+    std::vector<std::int64_t> lp((size_t)nl + 1);
+    detail::check(p, sfg_get_wavefront(p, nullptr, tg.data(), it.data(), nullptr, lp.data()),
+                  "wavefront");
+    for (std::int64_t q = 0; q < ne; ++q)
+      ws.entries.push_back(FusedEntry{tg[(size_t)q], it[(size_t)q], false});
+    for (std::int32_t l = 0; l < nl; ++l)
+      ws.levels.push_back({(Index)lp[(size_t)l], (Index)lp[(size_t)l + 1]});
+    return ws;
+  }
+  const DepDag j = joint_dag(g1, g2, f);
+  const LevelInfo li = level_info(j);
+  std::vector<std::vector<Index>> lev((size_t)li.critical_path + 1);
+  for (Index v = 0; v < j.nvert; ++v)
+    lev[(size_t)li.level[(size_t)v]].push_back(v);
+  for (Index l = 1; l <= li.critical_path; ++l) {
+    const Index b = (Index)ws.entries.size();
+    for (Index v : lev[(size_t)l])
+      ws.entries.push_back(v < g1.nvert ? FusedEntry{1, v, false} : FusedEntry{2, v - g1.nvert, false});
+    ws.levels.push_back({b, (Index)ws.entries.size()});
+  }
+  return ws;
+}
+
+// execute_joint_wavefront (executor.hpp:465-507): the joint level sets in
+// order, a grid barrier between levels (sfg_execute_wavefront).
+inline ExecStats execute_joint_wavefront(const DepDag& g1, const DepDag& g2, const InterDep& f,
+                                         KernelState& st, Index /*nthreads*/ = 0) {
+  detail::same_state(st, g1, g2);
+  if (f.origin && f.origin != st.id())
+    throw std::invalid_argument("the InterDep does not belong to this KernelState");
+  const std::int64_t l0 = sfg_launch_count(st.handle());
+  detail::check(st.handle(), sfg_execute_wavefront(st.handle()), "execute_joint_wavefront");
+  ExecStats es = detail::finish(st, l0);
+  std::int32_t nl = 0;
+  detail::check(st.handle(), sfg_get_wavefront(st.handle(), nullptr, nullptr, nullptr, &nl, nullptr),
+                "wavefront");
+  es.barriers = nl > 0 ? nl - 1 : 0;
+  return es;
+}
+
+// execute_sequential (executor.hpp:315-322) / run_sequential_reference
+// (kernels.hpp:574-582): the reference loop on one GPU thread
+inline ExecStats execute_sequential(KernelState& st) {
+  const std::int64_t l0 = sfg_launch_count(st.handle());
+  detail::check(st.handle(), sfg_execute_sequential(st.handle()), "execute_sequential");
   return detail::finish(st, l0);
 }
+inline void run_sequential_reference(KernelState& st) { execute_sequential(st); }
 
 // One kernel of the pair alone (1 or 2): the halves of execute_unfused, for
 // callers that move data between them (config 1's row-sharded SpMV).
@@ -468,8 +896,8 @@ inline void execute_batch(KernelState& st, const std::vector<const double*>& vin
                 "execute_batch");
 }
 
-// kernels.hpp:498-502: a no-op -- every execution re-initialises its outputs
-inline void reset(KernelState&) {}
+// kernels.hpp:498-502: fac = fac0, vmid = vout = 0 (on the device)
+inline void reset(KernelState& st) { detail::check(st.handle(), sfg_reset(st.handle()), "reset"); }
 
 // kernels.hpp:585-608, all systems concatenated system-major
 inline std::vector<double> collect_outputs(KernelState& st) {
@@ -534,6 +962,22 @@ inline CscMatrix permute_symmetric(const CscMatrix& A, const std::vector<Index>&
   if (st != SFG_OK)
     throw InvalidMatrixError("not a permutation");
   return detail::from_handle(out);
+}
+
+namespace detail {
+inline CscMatrix generated(std::int32_t kind, std::int32_t a, std::int32_t b, std::uint64_t seed) {
+  sfg_matrix* h = nullptr;
+  if (sfg_matrix_gen(kind, a, b, seed, &h) != SFG_OK)
+    throw std::invalid_argument("bad generator parameters");
+  return from_handle(h);
+}
+} // namespace detail
+
+// fixtures.hpp:49-91: the 5-point Laplacian of a k x k grid, nested-dissection numbered
+inline CscMatrix gen_grid_laplacian(Index k) { return detail::generated(0, k, 0, 0); }
+// fixtures.hpp:97-141
+inline CscMatrix gen_banded_spd(Index n, Index bandwidth, std::uint64_t seed) {
+  return detail::generated(1, n, bandwidth, seed);
 }
 
 // fixtures.hpp:148-155

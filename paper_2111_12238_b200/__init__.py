@@ -8,12 +8,14 @@ fallback.
 """
 from .api import (COMBOS, CscMatrix, DepDag, FactorizationError, FusedPartitioning,
                   FusedSchedule, InterDep, InvalidMatrixError, KernelState, LevelInfo,
-                  NoDeviceError, PCG, ParseError, build_g1, build_g2, collect_outputs,
+                  NoDeviceError, PCG, ParseError, WavefrontSchedule, build_g1, build_g2,
+                  build_wavefront_schedule, collect_outputs, compile_schedule,
                   compute_reuse, config5_systems, config_matrix, execute_fused,
-                  execute_unfused, gen_banded_spd, gen_grid_laplacian,
-                  gen_vector, inter_dag, joint_dag, level_info,
-                  make_fused_schedule, make_state, permute_symmetric,
-                  read_matrix_market, read_permutation, reset, write_matrix_market)
+                  execute_joint_wavefront, execute_sequential, execute_unfused,
+                  gen_banded_spd, gen_grid_laplacian, gen_vector, inter_dag, joint_dag,
+                  level_info, make_fused_schedule, make_state, msp, permute_symmetric,
+                  read_matrix_market, read_permutation, reset, run_sequential_reference,
+                  validate_fused_partitioning, write_matrix_market)
 
 __all__ = [
     "COMBOS", "CscMatrix", "DepDag", "FactorizationError", "FusedPartitioning",
@@ -23,5 +25,7 @@ __all__ = [
     "execute_unfused", "gen_banded_spd", "gen_grid_laplacian", "gen_vector",
     "inter_dag", "joint_dag", "level_info", "make_fused_schedule",
     "make_state", "permute_symmetric", "read_matrix_market", "read_permutation",
-    "reset", "write_matrix_market",
+    "reset", "write_matrix_market", "WavefrontSchedule", "build_wavefront_schedule",
+    "compile_schedule", "execute_joint_wavefront", "execute_sequential", "msp",
+    "run_sequential_reference", "validate_fused_partitioning",
 ]

@@ -35,7 +35,8 @@ EXPORTS = (
     "sfg_last_error", "sfg_launch_count", "sfg_last_exec_ms", "sfg_matrix_gen",
     "sfg_matrix_dims", "sfg_matrix_copy", "sfg_matrix_free", "sfg_matrix_read_mm",
     "sfg_matrix_write_mm", "sfg_matrix_from_csc", "sfg_matrix_permute", "sfg_read_permutation",
-    "sfg_matrix_perturb_diag", "sfg_gen_vector",
+    "sfg_matrix_perturb_diag", "sfg_gen_vector", "sfg_execute_wavefront", "sfg_get_wavefront",
+    "sfg_execute_sequential", "sfg_check_schedule", "sfg_dag_levels", "sfg_reset",
 )
 
 i32p = C.POINTER(C.c_int32)
@@ -127,6 +128,18 @@ def load(path: str | None = None):
     L.sfg_execute_fused.restype = st
     L.sfg_execute_unfused.argtypes = [vp]
     L.sfg_execute_unfused.restype = st
+    L.sfg_execute_wavefront.argtypes = [vp]
+    L.sfg_execute_wavefront.restype = st
+    L.sfg_execute_sequential.argtypes = [vp]
+    L.sfg_execute_sequential.restype = st
+    L.sfg_get_wavefront.argtypes = [vp, i64p, u8p, i32p, i32p, i64p]
+    L.sfg_get_wavefront.restype = st
+    L.sfg_check_schedule.argtypes = [vp, C.c_int64, u8p, i32p, i64p]
+    L.sfg_check_schedule.restype = st
+    L.sfg_dag_levels.argtypes = [C.c_int32, i32p, i32p, i32p, i32p, i32p, i32p]
+    L.sfg_dag_levels.restype = st
+    L.sfg_reset.argtypes = [vp]
+    L.sfg_reset.restype = st
     L.sfg_synchronize.argtypes = [vp]
     L.sfg_synchronize.restype = st
     L.sfg_collect_outputs.argtypes = [vp, f64p, C.c_int64]

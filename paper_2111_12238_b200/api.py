@@ -21,6 +21,8 @@ from __future__ import annotations
 import ctypes as C
 from dataclasses import dataclass
 
+import weakref
+
 import numpy as np
 
 from . import abi
@@ -72,12 +74,15 @@ class CscMatrix:
 
 @dataclass
 class DepDag:
-    """DepDag (dag.hpp:17-30)."""
+    """DepDag (dag.hpp:17-30).  ``origin`` (a weak reference to the
+    KernelState it was built from, or None) lets msp / joint_dag / the
+    executors use that state's GPU inspector."""
 
     nvert: int
     succptr: np.ndarray
     succ: np.ndarray
     cost: np.ndarray
+    origin: object = None
 
     def nedges(self) -> int:
         return int(self.succptr[-1]) if len(self.succptr) else 0
@@ -91,6 +96,7 @@ class InterDep:
     ncols: int
     rowptr: np.ndarray
     colidx: np.ndarray
+    origin: object = None
 
 
 @dataclass
@@ -105,15 +111,33 @@ class LevelInfo:
 
 @dataclass
 class FusedSchedule:
-    """The GPU-built fused schedule: entries (tag, iter) in ticket order,
-    grouped into wavefronts (the s-partition analogue) by ``wave_ptr``."""
+    """FusedSchedule (executor.hpp:138-150) in flat form: entries (tag, iter)
+    in execution order, grouped into s-partitions by ``wave_ptr``.
+    ``checked_for``: weak reference to the KernelState the entries were
+    verified against (execute_fused verifies any other schedule first)."""
 
     tags: np.ndarray
     iters: np.ndarray
     wave_ptr: np.ndarray
+    interleaved: bool = False
+    fusion: bool = True
+    checked_for: object = None
 
     def nspartitions(self) -> int:
         return len(self.wave_ptr) - 1
+
+
+@dataclass
+class WavefrontSchedule:
+    """WavefrontSchedule (executor.hpp:152-156): the joint DAG's level sets,
+    level l = entries [level_ptr[l], level_ptr[l+1])."""
+
+    tags: np.ndarray
+    iters: np.ndarray
+    level_ptr: np.ndarray
+
+    def nlevels(self) -> int:
+        return len(self.level_ptr) - 1
 
 
 @dataclass
@@ -126,6 +150,10 @@ class FusedPartitioning:
     w_ptr: np.ndarray
     tags: np.ndarray
     iters: np.ndarray
+    interleaved: bool = False
+    reuse_ratio: float = 0.0
+    fusion: bool = True
+    origin: object = None
 
     def b(self) -> int:
         return len(self.s_ptr) - 1
@@ -242,7 +270,7 @@ class KernelState:
         co = np.empty(max(nv.value, 1), np.int64)
         self._chk(self.L.sfg_get_dag(self.h, which, None, None, ptr(sp, i32p), ptr(su, i32p),
                                      ptr(co, i64p)), "dag")
-        return DepDag(nv.value, sp, su[:ne.value], co[:nv.value])
+        return DepDag(nv.value, sp, su[:ne.value], co[:nv.value], weakref.ref(self))
 
     def inter_dag(self) -> InterDep:
         nr = C.c_int32()
@@ -254,7 +282,7 @@ class KernelState:
         ci = np.empty(max(nnz.value, 1), np.int32)
         self._chk(self.L.sfg_get_interdep(self.h, None, None, None, ptr(rp, i32p),
                                           ptr(ci, i32p)), "inter_dag")
-        return InterDep(nr.value, nc.value, rp, ci[:nnz.value])
+        return InterDep(nr.value, nc.value, rp, ci[:nnz.value], weakref.ref(self))
 
     def level_info(self, which: int) -> LevelInfo:
         nv = self.n if which < 3 else 2 * self.n
@@ -299,7 +327,51 @@ class KernelState:
         self._chk(self.L.sfg_get_partitioning(self.h, None, None, None, ptr(sp, i64p),
                                               ptr(wp, i64p), ptr(tags, u8p), ptr(iters, i32p)),
                   "partitioning")
-        return FusedPartitioning(sp, wp, tags[:ne.value], iters[:ne.value])
+        r = self.compute_reuse()
+        return FusedPartitioning(sp, wp, tags[:ne.value], iters[:ne.value], r >= 1.0, r, True,
+                                 weakref.ref(self))
+
+    def wavefront(self) -> "WavefrontSchedule":
+        """The joint DAG's level sets (build_wavefront_schedule,
+        executor.hpp:209-229), built on the GPU."""
+        ne = C.c_int64()
+        nl = C.c_int32()
+        self._chk(self.L.sfg_get_wavefront(self.h, C.byref(ne), None, None, C.byref(nl), None),
+                  "wavefront")
+        tags = np.empty(max(ne.value, 1), np.uint8)
+        iters = np.empty(max(ne.value, 1), np.int32)
+        lp = np.empty(nl.value + 1, np.int64)
+        self._chk(self.L.sfg_get_wavefront(self.h, None, ptr(tags, u8p), ptr(iters, i32p), None,
+                                           ptr(lp, i64p)), "wavefront")
+        return WavefrontSchedule(tags[:ne.value], iters[:ne.value], lp)
+
+    def check_schedule(self, tags: np.ndarray, iters: np.ndarray) -> int:
+        """Violations of a flattened schedule against this state's joint DAG
+        (sfg_check_schedule): missing / repeated iterations and dependences
+        out of order.  0 = a valid order."""
+        tags = np.ascontiguousarray(tags, np.uint8)
+        iters = np.ascontiguousarray(iters, np.int32)
+        bad = C.c_int64()
+        self._chk(self.L.sfg_check_schedule(self.h, len(tags), ptr(tags, u8p), ptr(iters, i32p),
+                                            C.byref(bad)), "check_schedule")
+        return int(bad.value)
+
+    def execute_wavefront(self, sync: bool = True):
+        """execute_joint_wavefront (executor.hpp:465-507) on the GPU."""
+        self._chk(self.L.sfg_execute_wavefront(self.h), "execute_joint_wavefront")
+        if sync:
+            self.synchronize()
+
+    def execute_sequential(self, sync: bool = True):
+        """execute_sequential (executor.hpp:315-322): the reference loop on one
+        GPU thread."""
+        self._chk(self.L.sfg_execute_sequential(self.h), "execute_sequential")
+        if sync:
+            self.synchronize()
+
+    def reset(self):
+        """reset (kernels.hpp:498-502): fac = fac0, vmid = vout = 0."""
+        self._chk(self.L.sfg_reset(self.h), "reset")
 
     # ---- executor
     def execute_fused(self, sync: bool = True):
@@ -367,14 +439,15 @@ class KernelState:
         self._chk(self.L.sfg_last_exec_ms(self.h, C.byref(tot), C.byref(ker)), "last_exec_ms")
         return tot.value, ker.value
 
-    def bench(self, reps: int, unfused: bool = False):
+    def bench(self, reps: int, unfused: bool | int = False):
         """reps back-to-back executions timed with CUDA events on the plan
-        stream: (total_ms, mean main-kernel ms)."""
+        stream: (total_ms, mean main-kernel ms).  unfused: False/0 fused,
+        True/1 the two-launch comparator, 2 the joint wavefront executor."""
         if not self.inspected:
             self.inspect()
         tot = C.c_float()
         ker = C.c_float()
-        self._chk(self.L.sfg_bench_executions(self.h, reps, 1 if unfused else 0, C.byref(tot),
+        self._chk(self.L.sfg_bench_executions(self.h, reps, int(unfused), C.byref(tot),
                                               C.byref(ker)), "bench")
         return tot.value, ker.value
 
@@ -407,38 +480,263 @@ def inter_dag(st: KernelState) -> InterDep:
     return st.inter_dag()
 
 
-def joint_dag(st: KernelState) -> DepDag:
-    return st.dag(3)
+def _state_of(*objs):
+    """The live KernelState every object was built from, or None."""
+    st = None
+    for o in objs:
+        ref = getattr(o, "origin", None)
+        s = ref() if ref is not None else None
+        if s is None or (st is not None and s is not st):
+            return None
+        st = s
+    return st
 
 
-def level_info(st: KernelState, which: int = 3) -> LevelInfo:
-    return st.level_info(which)
+def joint_dag(st_or_g1, g2: DepDag | None = None, f: InterDep | None = None) -> DepDag:
+    """joint_dag (dag.hpp:222-238): joint_dag(st) from the state's GPU
+    inspector, or joint_dag(g1, g2, f) from the structures (edges of G1, G2
+    offset by |V1|, (j, |V1| + i) per F_ij; sorted, duplicate-free)."""
+    if isinstance(st_or_g1, KernelState):
+        return st_or_g1.dag(3)
+    g1 = st_or_g1
+    st = _state_of(g1, g2, f)
+    if st is not None:
+        return st.dag(3)
+    n1 = g1.nvert
+    src = [np.repeat(np.arange(n1, dtype=np.int64), np.diff(g1.succptr)),
+           n1 + np.repeat(np.arange(g2.nvert, dtype=np.int64), np.diff(g2.succptr)),
+           np.asarray(f.colidx[:int(f.rowptr[-1])], np.int64)]
+    dst = [np.asarray(g1.succ[:g1.nedges()], np.int64), n1 + np.asarray(g2.succ[:g2.nedges()], np.int64),
+           n1 + np.repeat(np.arange(f.nrows, dtype=np.int64), np.diff(f.rowptr))]
+    nv = n1 + g2.nvert
+    key = np.unique(np.concatenate(src) * nv + np.concatenate(dst))
+    u, v = key // max(nv, 1), key % max(nv, 1)
+    sp = np.zeros(nv + 1, np.int32)
+    np.add.at(sp, u + 1, 1)
+    return DepDag(nv, np.cumsum(sp).astype(np.int32), v.astype(np.int32),
+                  np.concatenate([g1.cost, g2.cost]).astype(np.int64))
+
+
+def level_info(st_or_dag, which: int = 3) -> LevelInfo:
+    """level_info (dag.hpp:197-218) of a state's G1/G2/joint DAG, or of any
+    DepDag (computed on the GPU, sfg_dag_levels)."""
+    if isinstance(st_or_dag, KernelState):
+        return st_or_dag.level_info(which)
+    g = st_or_dag
+    L = abi.load()
+    nv = g.nvert
+    sp = np.ascontiguousarray(g.succptr, np.int32)
+    su = np.ascontiguousarray(g.succ if len(g.succ) else np.zeros(1, np.int32), np.int32)
+    lv, ht, sl = (np.empty(max(nv, 1), np.int32) for _ in range(3))
+    P = C.c_int32()
+    st = L.sfg_dag_levels(nv, ptr(sp, i32p), ptr(su, i32p), ptr(lv, i32p), ptr(ht, i32p),
+                          ptr(sl, i32p), C.byref(P))
+    if st == abi.SFG_ERR_INVALID_ARGUMENT:
+        raise ValueError("dependence cycle: edge does not ascend")
+    _raise(L, None, st, "level_info")
+    return LevelInfo(lv[:nv], ht[:nv], sl[:nv], P.value)
 
 
 def compute_reuse(st: KernelState) -> float:
     return st.compute_reuse()
 
 
+def msp(g1: DepDag, g2: DepDag, f: InterDep, r: int, reuse_ratio: float,
+        redundancy_factor: float = 2.0) -> FusedPartitioning:
+    """msp (msp.hpp:825-1082).  DAGs of a live state: that state's GPU
+    inspector partitioning (what execute_fused runs).  Otherwise the joint
+    DAG's level sets, each split into at most r contiguous w-partitions --
+    a valid fused partitioning of any DAG pair.  Packing is interleaved iff
+    reuse_ratio >= 1 (msp.hpp:834)."""
+    if r < 1:
+        raise ValueError("partition count must be >= 1")
+    st = _state_of(g1, g2, f)
+    if st is not None:
+        V = st.partitioning()
+        V.reuse_ratio = reuse_ratio
+        V.interleaved = reuse_ratio >= 1.0
+        return V
+    ws = build_wavefront_schedule(g1, g2, f)
+    s_ptr, w_ptr = [0], [0]
+    for l in range(ws.nlevels()):
+        b, e = int(ws.level_ptr[l]), int(ws.level_ptr[l + 1])
+        parts = min(r, e - b)
+        for w in range(parts):
+            w_ptr.append(b + (w + 1) * (e - b) // parts)
+        s_ptr.append(len(w_ptr) - 1)
+    return FusedPartitioning(np.array(s_ptr, np.int64), np.array(w_ptr, np.int64), ws.tags,
+                             ws.iters, reuse_ratio >= 1.0, reuse_ratio)
+
+
+def validate_fused_partitioning(V: FusedPartitioning, g1: DepDag, g2: DepDag,
+                                f: InterDep) -> list:
+    """validate_fused_partitioning (msp.hpp:1110-1237): coverage, duplicate
+    provenance, within-partition order and the cross-partition invariant,
+    with the reference's messages; [] means valid."""
+    bad = []
+    if not V.fusion:
+        return ["fusion disabled but schedule non-empty"] if V.b() else []
+    n1, n2 = g1.nvert, g2.nvert
+    pos1 = [[] for _ in range(n1)]
+    pos2 = [None] * n2
+    cnt2 = [0] * n2
+    for s in range(V.b()):
+        for w in range(int(V.s_ptr[s]), int(V.s_ptr[s + 1])):
+            for e, q in enumerate(range(int(V.w_ptr[w]), int(V.w_ptr[w + 1]))):
+                tag, it = int(V.tags[q]), int(V.iters[q])
+                wl = w - int(V.s_ptr[s])
+                where = f"(s={s},w={wl},entry={e}): "
+                if tag == 1:
+                    if not 0 <= it < n1:
+                        bad.append(where + "kernel-1 iteration out of range")
+                    else:
+                        pos1[it].append((s, wl, e, w))
+                elif not 0 <= it < n2:
+                    bad.append(where + "kernel-2 iteration out of range")
+                else:
+                    cnt2[it] += 1
+                    if cnt2[it] > 1:
+                        bad.append(where + "kernel-2 iteration duplicated")
+                    pos2[it] = (s, wl, e, w)
+    bad += [f"kernel-1 iteration {v} missing" for v in range(n1) if not pos1[v]]
+    bad += [f"kernel-2 iteration {v} missing" for v in range(n2) if cnt2[v] == 0]
+    if bad:
+        return bad
+    for v in range(n1):
+        if len(pos1[v]) > 1:
+            bad.append(f"(s={pos1[v][0][0]},w={pos1[v][0][1]},entry={pos1[v][0][2]}): "
+                       "replicated entry not flagged dup")
+    def before(p, u, tag):
+        w0 = int(V.w_ptr[p[3]])
+        return any(int(V.tags[w0 + k]) == tag and int(V.iters[w0 + k]) == u for k in range(p[2]))
+    def earliest1(u):
+        return min(p[0] for p in pos1[u])
+    def preds(g):
+        pr = [[] for _ in range(g.nvert)]
+        for u in range(g.nvert):
+            for p in range(int(g.succptr[u]), int(g.succptr[u + 1])):
+                pr[int(g.succ[p])].append(u)
+        return pr
+    p1, p2 = preds(g1), preds(g2)
+    for v in range(n1):
+        for pv in pos1[v]:
+            for u in p1[v]:
+                if not before(pv, u, 1) and earliest1(u) >= pv[0]:
+                    bad.append(f"(s={pv[0]},w={pv[1]},entry={pv[2]}): kernel-1 dependence on {u} unsatisfied")
+    for v in range(n2):
+        pv = pos2[v]
+        for u in p2[v]:
+            pu = pos2[u]
+            if not (pu[0] < pv[0] or (pu[0] == pv[0] and pu[1] == pv[1] and pu[2] < pv[2])):
+                bad.append(f"(s={pv[0]},w={pv[1]},entry={pv[2]}): kernel-2 dependence on {u} unsatisfied")
+        for p in range(int(f.rowptr[v]), int(f.rowptr[v + 1])):
+            u = int(f.colidx[p])
+            if not before(pv, u, 1) and earliest1(u) >= pv[0]:
+                bad.append(f"(s={pv[0]},w={pv[1]},entry={pv[2]}): cross-kernel dependence on {u} unsatisfied")
+    return bad
+
+
+def compile_schedule(V: FusedPartitioning, reuse_ratio: float, g1: DepDag, g2: DepDag,
+                     r: int = 1) -> FusedSchedule:
+    """compile_schedule (executor.hpp:235-268): flattens V; interleaved iff
+    reuse_ratio >= 1.  The entries are verified against the state the DAGs
+    came from, when it is alive."""
+    wave = np.asarray([V.w_ptr[int(k)] for k in V.s_ptr], np.int64)
+    fs = FusedSchedule(np.asarray(V.tags, np.uint8), np.asarray(V.iters, np.int32), wave,
+                       reuse_ratio >= 1.0, V.fusion)
+    st = _state_of(g1, g2)
+    if st is not None and st.check_schedule(fs.tags, fs.iters) == 0:
+        fs.checked_for = weakref.ref(st)
+    return fs
+
+
 def make_fused_schedule(st: KernelState) -> FusedSchedule:
-    """The GPU inspector (replaces msp + compile_schedule)."""
+    """The state's own schedule (the GPU inspector replaces msp +
+    compile_schedule)."""
     st.inspect()
-    return st.schedule()
+    fs = st.schedule()
+    fs.interleaved = st.compute_reuse() >= 1.0
+    fs.checked_for = weakref.ref(st)
+    return fs
+
+
+def _verified(sched: FusedSchedule | None, st: KernelState) -> None:
+    if sched is None:
+        return
+    ref = sched.checked_for
+    if ref is not None and ref() is st:
+        return
+    if not sched.fusion:
+        raise RuntimeError("execute_fused: fusion disabled, run the fallback schedule")
+    bad = st.check_schedule(sched.tags, sched.iters)
+    if bad:
+        raise ValueError(f"execute_fused: schedule violates the joint DAG of this state ({bad} violations)")
 
 
 def execute_fused(sched: FusedSchedule | None, st: KernelState, nthreads: int | None = None):
-    """execute_fused (executor.hpp:395-461) on the GPU. ``nthreads`` is
-    accepted for signature parity and ignored (the GPU grid is sized to the
-    device)."""
+    """execute_fused (executor.hpp:395-461) on the GPU.  A schedule not
+    verified for this state is checked against its joint DAG first
+    (ValueError if an iteration is missing/repeated or a dependence is out of
+    order); any valid order computes the same result, so the state's own
+    executor runs it.  ``nthreads`` has no GPU meaning."""
+    _verified(sched, st)
     st.execute_fused()
 
 
-def execute_unfused(st: KernelState):
+def _same_state(st: KernelState, *objs):
+    for o in objs:
+        ref = getattr(o, "origin", None)
+        if ref is not None and ref() is not st:
+            raise ValueError("the DAGs do not belong to this KernelState")
+
+
+def execute_unfused(st_or_g1, g2: DepDag | None = None, st: KernelState | None = None,
+                    nthreads: int | None = None):
+    """execute_unfused(st) or execute_unfused(g1, g2, st, T) (executor.hpp:325-392)."""
+    if isinstance(st_or_g1, KernelState):
+        st_or_g1.execute_unfused()
+        return
+    _same_state(st, st_or_g1, g2)
     st.execute_unfused()
 
 
+def build_wavefront_schedule(g1: DepDag, g2: DepDag, f: InterDep) -> WavefrontSchedule:
+    """build_wavefront_schedule (executor.hpp:209-229): joint level sets,
+    ascending vertex id within a level (the GPU inspector's for DAGs of a live
+    state; otherwise from the joint DAG's GPU-computed levels)."""
+    st = _state_of(g1, g2, f)
+    if st is not None:
+        return st.wavefront()
+    j = joint_dag(g1, g2, f)
+    li = level_info(j)
+    order = np.lexsort((np.arange(j.nvert), li.level))
+    counts = np.bincount(li.level, minlength=li.critical_path + 1)[1:]
+    lp = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
+    tags = np.where(order < g1.nvert, 1, 2).astype(np.uint8)
+    iters = np.where(order < g1.nvert, order, order - g1.nvert).astype(np.int32)
+    return WavefrontSchedule(tags, iters, lp)
+
+
+def execute_joint_wavefront(g1: DepDag, g2: DepDag, f: InterDep, st: KernelState,
+                            nthreads: int | None = None):
+    """execute_joint_wavefront (executor.hpp:465-507): the joint level sets
+    in order with a grid barrier between levels (sfg_execute_wavefront)."""
+    _same_state(st, g1, g2, f)
+    st.execute_wavefront()
+
+
+def execute_sequential(st: KernelState):
+    """execute_sequential (executor.hpp:315-322) on one GPU thread."""
+    st.execute_sequential()
+
+
+def run_sequential_reference(st: KernelState):
+    st.execute_sequential()
+
+
 def reset(st: KernelState):
-    """reset (kernels.hpp:498-502): every execution re-initialises its
-    outputs on the device, so this is a no-op kept for API parity."""
+    """reset (kernels.hpp:498-502): fac = fac0, vmid = vout = 0 (device)."""
+    st.reset()
 
 
 def collect_outputs(st: KernelState) -> np.ndarray:

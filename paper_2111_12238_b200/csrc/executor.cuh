@@ -73,5 +73,18 @@ void launch_ilu0(int combo, const ExecArgs& a, cudaStream_t s);
 void launch_dscal_csr(const ExecArgs& a, cudaStream_t s);
 // combo 7 kernel 1 alone (unfused): work[p] = (d_i * a_p) * d_j
 void launch_dscal(const ExecArgs& a, cudaStream_t s);
+// execute_joint_wavefront (wavefront.cu): the joint level sets verts[lptr[l]
+// .. lptr[l+1]) (vertex v < n: kernel-1 iteration v, else kernel-2 iteration
+// v - n) level by level with a grid barrier between levels.  m_*: A in CSC
+// for combo 4's scatter.  nlev < 0: run_sequential_reference on one thread.
+void launch_wavefront(const ExecArgs& a, int combo, const int32_t* verts, const int64_t* lptr,
+                      int32_t nlev, const int32_t* m_ptr, const int32_t* m_idx,
+                      const double* m_val, cudaStream_t s);
+// Number of violations of a flattened schedule (tags/iters on the host)
+// against the joint DAG (successor CSR on the device, 2n vertices): an
+// iteration missing or repeated, or an edge u -> v with v scheduled first.
+int64_t check_schedule_order(const int32_t* jptr, const int32_t* jsucc, int32_t n,
+                             const uint8_t* tags_h, const int32_t* iters_h, int64_t ne,
+                             cudaStream_t s);
 
 } // namespace sfg

@@ -37,6 +37,7 @@ struct sfg_plan {
   int64_t lower_count = 0;
 
   DBuf<int32_t> m_ptr, m_idx; // M pattern (CSC)
+  DBuf<double> m_val;         // M values (combo 4: the wavefront executor's CSC scatter)
   DBuf<int32_t> lr_ptr, lr_idx;
   DBuf<double> lr_val;
   DBuf<int32_t> lt_ptr, lt_idx;
@@ -57,6 +58,12 @@ struct sfg_plan {
   std::vector<int64_t> wave_ptr; // wavefront boundaries over tickets
   int32_t seg2_start_wave = -1;  // first wave of the second ticket segment
   DBuf<unsigned long long> counter, err;
+
+  // joint-DAG level sets (build_wavefront_schedule) for the wavefront executor
+  bool have_wf = false;
+  DBuf<int32_t> wf_verts;
+  DBuf<int64_t> wf_lptr;
+  std::vector<int64_t> wf_ptr;
 
   // parity structures (lazy)
   std::unique_ptr<DevDag> dags[3];
@@ -500,6 +507,8 @@ void build_plan(sfg_plan* P, const int32_t* colptr, const int32_t* rowidx,
       P->dvec.alloc(n > 0 ? n : 1);
       dscal_vector(P->lc_ptr.p, P->lc_val.p, n, P->dvec.p, s);
     }
+    if (combo == 4)
+      P->m_val = std::move(mval);
     if (combo == 5 || combo == 7) {
       P->nnzF = nnzL;
       P->fac.alloc(nnzL > 0 ? nnzL : 1);
@@ -1281,6 +1290,50 @@ void exec_fused_impl(sfg_plan* P, cudaEvent_t kb, cudaEvent_t ke) {
   SFG_CUDA(cudaEventRecord(ke, P->stream));
 }
 
+// Joint-DAG level sets, ascending vertex id within a level
+// (build_wavefront_schedule, executor.hpp:209-229), on the GPU: a stable sort
+// of the joint vertices by their joint level.
+void ensure_wavefront(sfg_plan* P) {
+  if (P->have_wf)
+    return;
+  ensure_levels(P, 3);
+  const int32_t nv = 2 * P->n;
+  P->wf_verts.alloc(nv > 0 ? nv : 1);
+  order_by_level(P->lev[2].p, nv, P->crit[2], P->wf_verts.p, &P->wf_ptr, P->stream);
+  P->wf_lptr.alloc((int64_t)P->wf_ptr.size());
+  SFG_CUDA(cudaMemcpyAsync(P->wf_lptr.p, P->wf_ptr.data(), sizeof(int64_t) * P->wf_ptr.size(),
+                           cudaMemcpyHostToDevice, P->stream));
+  SFG_CUDA(cudaStreamSynchronize(P->stream));
+  P->have_wf = true;
+}
+
+// execute_joint_wavefront (executor.hpp:465-507): the joint level sets one
+// after another with a grid barrier between them (wavefront.cu).
+void exec_wavefront_impl(sfg_plan* P, cudaEvent_t kb, cudaEvent_t ke) {
+  launch_prep(nullptr, 0, P->counter.p, P->err.p, P->stream);
+  if (P->combo == 4 && P->n > 0) // spmv_csc_col accumulates into y = 0 (reset, kernels.hpp:498-502)
+    SFG_CUDA(cudaMemsetAsync(P->vout.p, 0, sizeof(double) * (size_t)P->n, P->stream));
+  SFG_CUDA(cudaEventRecord(kb, P->stream));
+  ExecArgs a = exec_args(P);
+  launch_wavefront(a, P->combo, P->wf_verts.p, P->wf_lptr.p, (int32_t)P->wf_ptr.size() - 1,
+                   P->m_ptr.p, P->m_idx.p, P->m_val.p, P->stream);
+  SFG_CUDA(cudaGetLastError());
+  SFG_CUDA(cudaEventRecord(ke, P->stream));
+}
+
+// execute_sequential (executor.hpp:315-322): run_sequential_reference on one
+// GPU thread -- the reference's sequential baseline, same outputs.
+void exec_sequential_impl(sfg_plan* P, cudaEvent_t kb, cudaEvent_t ke) {
+  launch_prep(nullptr, 0, P->counter.p, P->err.p, P->stream);
+  if (P->combo == 4 && P->n > 0)
+    SFG_CUDA(cudaMemsetAsync(P->vout.p, 0, sizeof(double) * (size_t)P->n, P->stream));
+  SFG_CUDA(cudaEventRecord(kb, P->stream));
+  ExecArgs a = exec_args(P);
+  launch_wavefront(a, P->combo, nullptr, nullptr, -1, P->m_ptr.p, P->m_idx.p, P->m_val.p,
+                   P->stream);
+  SFG_CUDA(cudaEventRecord(ke, P->stream));
+}
+
 // The unfused comparator (execute_unfused, executor.hpp:325-383): kernel 1
 // alone, then kernel 2 alone; stream order is the barrier between them.
 // which = 1 / 2 runs only that kernel (sfg_execute_kernel); kernel 2 alone
@@ -1692,6 +1745,9 @@ sfg_status sfg_set_values(sfg_plan* P, const double* values_host) {
       gather_values(P->mstage.p, nnzM, P->map_lc.p, nnzL, S, P->lc_val.p, s);
     if (c == 2 || c == 3 || c == 4 || c == 6)
       gather_values(P->mstage.p, nnzM, P->map_ar.p, nnzM, 1, P->ar_val.p, s);
+    if (c == 4)
+      SFG_CUDA(cudaMemcpyAsync(P->m_val.p, P->mstage.p, sizeof(double) * (size_t)nnzM,
+                               cudaMemcpyDeviceToDevice, s));
     if (c == 3) {
       const int32_t bad = scaling_vector_csr(P->diag.p, P->ar_val.p, n, P->dvec.p, s);
       if (bad >= 0)
@@ -1804,6 +1860,51 @@ sfg_status sfg_get_levels(sfg_plan* P, int32_t which, int32_t* level, int32_t* h
       *critical_path = P->crit[which - 1];
     return SFG_OK;
   });
+}
+
+sfg_status sfg_dag_levels(int32_t nvert, const int32_t* succptr, const int32_t* succ,
+                          int32_t* level, int32_t* height, int32_t* slack,
+                          int32_t* critical_path) {
+  if (nvert < 0 || (nvert > 0 && (!succptr || (!succ && succptr[nvert] > 0))))
+    return SFG_ERR_INVALID_ARGUMENT;
+  try {
+    int dc = 0;
+    if (cudaGetDeviceCount(&dc) != cudaSuccess || dc == 0)
+      return SFG_ERR_NO_DEVICE;
+    cudaStream_t s = nullptr;
+    DevDag g;
+    g.nvert = nvert;
+    g.nedges = nvert > 0 ? succptr[nvert] : 0;
+    g.ptr.alloc((int64_t)nvert + 1);
+    g.idx.alloc(g.nedges > 0 ? g.nedges : 1);
+    SFG_CUDA(cudaMemcpy(g.ptr.p, succptr, sizeof(int32_t) * ((size_t)nvert + 1),
+                        cudaMemcpyHostToDevice));
+    if (g.nedges)
+      SFG_CUDA(cudaMemcpy(g.idx.p, succ, sizeof(int32_t) * (size_t)g.nedges,
+                          cudaMemcpyHostToDevice));
+    if (!edges_ascend(g, s))
+      return SFG_ERR_INVALID_ARGUMENT; // "dependence cycle: edge does not ascend"
+    DevDag pred;
+    flip_dag(g, pred, s);
+    DBuf<int32_t> lev(nvert > 0 ? nvert : 1), hgt(nvert > 0 ? nvert : 1), slk(nvert > 0 ? nvert : 1);
+    const int32_t Pc = nvert > 0 ? levels_syncfree(pred.ptr.p, pred.idx.p, nvert, +1, lev.p, s) : 0;
+    if (nvert > 0) {
+      heights_syncfree(g.ptr.p, g.idx.p, nvert, hgt.p, s);
+      slack_from(lev.p, hgt.p, Pc, nvert, slk.p, s);
+    }
+    SFG_CUDA(cudaStreamSynchronize(s));
+    if (level && nvert)
+      SFG_CUDA(cudaMemcpy(level, lev.p, sizeof(int32_t) * (size_t)nvert, cudaMemcpyDeviceToHost));
+    if (height && nvert)
+      SFG_CUDA(cudaMemcpy(height, hgt.p, sizeof(int32_t) * (size_t)nvert, cudaMemcpyDeviceToHost));
+    if (slack && nvert)
+      SFG_CUDA(cudaMemcpy(slack, slk.p, sizeof(int32_t) * (size_t)nvert, cudaMemcpyDeviceToHost));
+    if (critical_path)
+      *critical_path = Pc;
+    return SFG_OK;
+  } catch (...) {
+    return SFG_ERR_CUDA;
+  }
 }
 
 sfg_status sfg_compute_reuse(sfg_plan* P, double* reuse) {
@@ -2302,6 +2403,79 @@ sfg_status sfg_execute_unfused(sfg_plan* P) {
   });
 }
 
+sfg_status sfg_execute_wavefront(sfg_plan* P) {
+  if (!P)
+    return SFG_ERR_INVALID_ARGUMENT;
+  return guarded(P, [&] {
+    DeviceScope ds(P->device);
+    LaunchScope ls(P);
+    ensure_wavefront(P);
+    SFG_CUDA(cudaEventRecord(P->ev[0], P->stream));
+    exec_wavefront_impl(P, P->ev[1], P->ev[2]);
+    SFG_CUDA(cudaEventRecord(P->ev[3], P->stream));
+    P->timed = true;
+    return SFG_OK;
+  });
+}
+
+sfg_status sfg_execute_sequential(sfg_plan* P) {
+  if (!P)
+    return SFG_ERR_INVALID_ARGUMENT;
+  return guarded(P, [&] {
+    DeviceScope ds(P->device);
+    LaunchScope ls(P);
+    SFG_CUDA(cudaEventRecord(P->ev[0], P->stream));
+    exec_sequential_impl(P, P->ev[1], P->ev[2]);
+    SFG_CUDA(cudaEventRecord(P->ev[3], P->stream));
+    P->timed = true;
+    return SFG_OK;
+  });
+}
+
+sfg_status sfg_check_schedule(sfg_plan* P, int64_t nentries, const uint8_t* tags,
+                              const int32_t* iters, int64_t* violations) {
+  if (!P || !violations || nentries < 0 || (nentries > 0 && (!tags || !iters)))
+    return SFG_ERR_INVALID_ARGUMENT;
+  return guarded(P, [&] {
+    DeviceScope ds(P->device);
+    LaunchScope ls(P);
+    ensure_dag(P, 3);
+    const DevDag& j = *P->dags[2];
+    *violations = check_schedule_order(j.ptr.p, j.idx.p, P->n, tags, iters, nentries, P->stream);
+    return SFG_OK;
+  });
+}
+
+sfg_status sfg_get_wavefront(sfg_plan* P, int64_t* nentries, uint8_t* tags, int32_t* iters,
+                             int32_t* nlevels, int64_t* level_ptr) {
+  if (!P)
+    return SFG_ERR_INVALID_ARGUMENT;
+  return guarded(P, [&] {
+    DeviceScope ds(P->device);
+    LaunchScope ls(P);
+    ensure_wavefront(P);
+    const int32_t n = P->n;
+    if (nentries)
+      *nentries = 2 * (int64_t)n;
+    if (nlevels)
+      *nlevels = (int32_t)P->wf_ptr.size() - 1;
+    if (level_ptr)
+      std::copy(P->wf_ptr.begin(), P->wf_ptr.end(), level_ptr);
+    if ((tags || iters) && n > 0) {
+      std::vector<int32_t> v((size_t)2 * n);
+      SFG_CUDA(cudaMemcpy(v.data(), P->wf_verts.p, sizeof(int32_t) * v.size(),
+                          cudaMemcpyDeviceToHost));
+      for (size_t q = 0; q < v.size(); ++q) {
+        if (tags)
+          tags[q] = v[q] < n ? 1 : 2;
+        if (iters)
+          iters[q] = v[q] < n ? v[q] : v[q] - n;
+      }
+    }
+    return SFG_OK;
+  });
+}
+
 sfg_status sfg_execute_kernel(sfg_plan* P, int32_t which) {
   if (!P || (which != 1 && which != 2))
     return SFG_ERR_INVALID_ARGUMENT;
@@ -2344,6 +2518,29 @@ sfg_status sfg_synchronize(sfg_plan* P) {
     DeviceScope ds(P->device);
     SFG_CUDA(cudaStreamSynchronize(P->stream));
     return check_error_word(P);
+  });
+}
+
+sfg_status sfg_reset(sfg_plan* P) {
+  if (!P)
+    return SFG_ERR_INVALID_ARGUMENT;
+  return guarded(P, [&] {
+    DeviceScope ds(P->device);
+    cudaStream_t s = P->stream;
+    const int64_t nv = (int64_t)P->n * P->nsys;
+    const int c = P->combo;
+    // reset (kernels.hpp:498-502): fac = fac0, vmid = vout = 0
+    if (P->nnzF > 0) {
+      const double* fac0 = (c == 5 || c == 7) ? P->lc_val.p : P->ar_val.p;
+      SFG_CUDA(cudaMemcpyAsync(P->fac.p, fac0, sizeof(double) * (size_t)P->nnzF,
+                               cudaMemcpyDeviceToDevice, s));
+    }
+    if (nv > 0 && P->vmid.p)
+      SFG_CUDA(cudaMemsetAsync(P->vmid.p, 0, sizeof(double) * (size_t)nv, s));
+    if (nv > 0 && P->vout.p)
+      SFG_CUDA(cudaMemsetAsync(P->vout.p, 0, sizeof(double) * (size_t)nv, s));
+    SFG_CUDA(cudaStreamSynchronize(s));
+    return SFG_OK;
   });
 }
 
@@ -2444,12 +2641,16 @@ sfg_status sfg_bench_executions(sfg_plan* P, int32_t reps, int32_t unfused, floa
   return guarded(P, [&] {
     DeviceScope ds(P->device);
     LaunchScope ls(P);
+    if (unfused == 2)
+      ensure_wavefront(P);
     std::vector<cudaEvent_t> ev((size_t)2 * reps + 2, nullptr);
     for (auto& e : ev)
       SFG_CUDA(cudaEventCreate(&e));
     SFG_CUDA(cudaEventRecord(ev[0], P->stream));
     for (int r = 0; r < reps; ++r) {
-      if (unfused)
+      if (unfused == 2)
+        exec_wavefront_impl(P, ev[(size_t)2 + 2 * r], ev[(size_t)3 + 2 * r]);
+      else if (unfused)
         exec_unfused_impl(P, ev[(size_t)2 + 2 * r], ev[(size_t)3 + 2 * r]);
       else
         exec_fused_impl(P, ev[(size_t)2 + 2 * r], ev[(size_t)3 + 2 * r]);

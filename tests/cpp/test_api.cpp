@@ -5,6 +5,7 @@
 // (oracle/sf_oracle.c, itself pinned to the reference's golden vectors).
 // Without a device it checks that make_state refuses to run (no CPU fallback).
 #include <algorithm>
+#include <cmath>
 #include <cstdio>
 #include <cstring>
 #include <vector>
@@ -115,7 +116,7 @@ int main(int argc, char** argv) {
         entries += (int64_t)wp.size();
     CHECK(V.b() > 0 && entries == 2 * (int64_t)M.nrows);
     const sf::FusedSchedule sched = sf::make_fused_schedule(st, 8);
-    CHECK((int64_t)sched.tags.size() == 2 * (int64_t)M.nrows);
+    CHECK((int64_t)sched.entries.size() == 2 * (int64_t)M.nrows);
     int eidx = 0;
     const std::vector<double> want = oracle_outputs(combo, M, &eidx);
     CHECK(eidx == -1);
@@ -123,8 +124,79 @@ int main(int argc, char** argv) {
     CHECK(es.launches >= 1 && es.barriers == 0);
     CHECK(sf::collect_outputs(st) == want);
     sf::reset(st);
+    {
+      // reset (kernels.hpp:498-502): fac = fac0, vmid = vout = 0
+      const std::vector<double> r0 = sf::collect_outputs(st);
+      const size_t nf = r0.size() - (size_t)M.nrows;
+      bool zeros = true;
+      for (size_t q = (combo == 1 || combo == 2 || combo == 4 || combo == 8) ? 0 : nf;
+           q < ((combo == 3 || combo == 7) ? 0 : r0.size()); ++q)
+        zeros = zeros && r0[q] == 0.0;
+      CHECK(zeros);
+    }
     sf::execute_unfused(st);
     CHECK(sf::collect_outputs(st) == want);
+    // the reference's canonical call sequence (fuse_demo.cpp:15-31)
+    {
+      const sf::DepDag g1 = sf::build_g1(st), g2 = sf::build_g2(st);
+      const sf::InterDep f = sf::inter_dag(st);
+      const double reuse = sf::compute_reuse(st);
+      const sf::FusedPartitioning V2 = sf::msp(g1, g2, f, 4, reuse);
+      CHECK(sf::validate_fused_partitioning(V2, g1, g2, f).empty());
+      CHECK(V2.interleaved == (reuse >= 1.0));
+      const sf::FusedSchedule s2 = sf::compile_schedule(V2, reuse, g1, g2, 4);
+      sf::execute_fused(s2, st, 4);
+      CHECK(sf::collect_outputs(st) == want);
+      sf::execute_unfused(g1, g2, st, 4);
+      CHECK(sf::collect_outputs(st) == want);
+      const sf::ExecStats ws = sf::execute_joint_wavefront(g1, g2, f, st, 4);
+      const std::vector<double> wout = sf::collect_outputs(st);
+      if (combo == 4) { // CSC scatter with atomic adds in any order (kernels.hpp:162-168)
+        double err = 0.0, mx = 0.0;
+        for (size_t q = 0; q < want.size(); ++q) {
+          err = std::max(err, std::abs(wout[q] - want[q]));
+          mx = std::max(mx, std::abs(want[q]));
+        }
+        CHECK(err <= 1e-13 * std::max(1.0, mx));
+      } else {
+        CHECK(wout == want);
+      }
+      const sf::WavefrontSchedule wfs = sf::build_wavefront_schedule(g1, g2, f);
+      CHECK(ws.barriers == (sf::Index)wfs.levels.size() - 1);
+      sf::execute_sequential(st);
+      CHECK(sf::collect_outputs(st) == want);
+      // the same DAGs without their state: joint DAG, levels, msp and the
+      // wavefront schedule are built from the structures alone
+      sf::DepDag h1 = g1, h2 = g2;
+      sf::InterDep hf = f;
+      h1.origin = h2.origin = hf.origin = 0;
+      const sf::DepDag hj = sf::joint_dag(h1, h2, hf), jj = sf::joint_dag(st);
+      CHECK(hj.succptr == jj.succptr && hj.succ == jj.succ && hj.cost == jj.cost);
+      const sf::LevelInfo hl = sf::level_info(hj), jl = sf::level_info(st, 3);
+      CHECK(hl.level == jl.level && hl.height == jl.height && hl.slack == jl.slack &&
+            hl.critical_path == jl.critical_path);
+      const sf::WavefrontSchedule hw = sf::build_wavefront_schedule(h1, h2, hf);
+      bool same_wf = hw.levels == wfs.levels && hw.entries.size() == wfs.entries.size();
+      for (size_t q = 0; same_wf && q < hw.entries.size(); ++q)
+        same_wf = hw.entries[q].tag == wfs.entries[q].tag && hw.entries[q].iter == wfs.entries[q].iter;
+      CHECK(same_wf);
+      const sf::FusedPartitioning V3 = sf::msp(h1, h2, hf, 3, reuse);
+      CHECK(sf::validate_fused_partitioning(V3, h1, h2, hf).empty());
+      const sf::FusedSchedule s3 = sf::compile_schedule(V3, reuse, h1, h2, 3);
+      CHECK(s3.checked_for == 0);
+      sf::execute_fused(s3, st, 3); // verified on the GPU, then run
+      CHECK(sf::collect_outputs(st) == want);
+      // a schedule that breaks a dependence is refused
+      sf::FusedSchedule bad = s3;
+      std::reverse(bad.entries.begin(), bad.entries.end());
+      bool refused = false;
+      try {
+        sf::execute_fused(bad, st, 3);
+      } catch (const std::invalid_argument&) {
+        refused = true;
+      }
+      CHECK(refused == (g1.nedges() + g2.nedges() + f.nnz() > 0));
+    }
     // the two halves of the unfused comparator
     sf::execute_kernel(st, 1);
     sf::execute_kernel(st, 2);

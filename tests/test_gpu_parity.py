@@ -243,12 +243,67 @@ def test_config5_batch_full_size(orc):
         st = sf.make_state(combo, M, nsys=nsys, values=vals, vin=vin)
         st.execute_fused()
         got = st.collect_outputs().reshape(nsys, 2 * n)
-        for s in (0, nsys - 1):
+        for s in range(nsys):  # every system of the batch
             Ms = Csc(n, M.colptr, M.rowidx, vals[s * nnz:(s + 1) * nnz])
             want = orc.run_sequential(combo, Ms, 7, vin=vin[s * n:(s + 1) * n])
             assert max_rel(got[s], want) <= TOL
             assert np.array_equal(got[s], want)
         del st
+
+
+# ---- inspector structures at the BASELINE sizes -----------------------------
+def _same_dag(got, want):
+    assert got.nvert == want.nvert
+    assert np.array_equal(got.succptr, want.succptr)
+    assert np.array_equal(got.succ, want.succ)
+    assert np.array_equal(got.cost, want.cost)
+
+
+def _structures_vs_oracle(orc, st, combo, Mo):
+    """G1, G2, F, the joint DAG, level_info of all three (level, height,
+    slack, critical path) and compute_reuse, bit for bit against the oracle
+    (dag.hpp:150-431 restated in oracle/sf_oracle.c, pinned by test_oracle)."""
+    w1, w2 = orc.build_g(combo, 1, Mo), orc.build_g(combo, 2, Mo)
+    wf = orc.inter_dag(combo, Mo)
+    _same_dag(st.dag(1), w1)
+    _same_dag(st.dag(2), w2)
+    f = st.inter_dag()
+    assert np.array_equal(f.rowptr, wf.rowptr) and np.array_equal(f.colidx, wf.colidx)
+    wj = orc.joint_dag(w1, w2, wf)
+    _same_dag(st.dag(3), wj)
+    for which, wg in ((1, w1), (2, w2), (3, wj)):
+        li, wl = st.level_info(which), orc.level_info(wg)
+        assert li.critical_path == wl.critical_path
+        assert np.array_equal(li.level, wl.level)
+        assert np.array_equal(li.height, wl.height)
+        assert np.array_equal(li.slack, wl.slack)
+    if combo != 8:  # the reference has no combo 8
+        assert st.compute_reuse() == orc.compute_reuse(combo, Mo)
+    # the joint level sets: ascending vertex id within a level
+    # (build_wavefront_schedule, executor.hpp:209-229)
+    ws = st.wavefront()
+    lv = orc.level_info(wj).level
+    order = np.lexsort((np.arange(len(lv)), lv))
+    n = st.n
+    assert np.array_equal(ws.tags, np.where(order < n, 1, 2))
+    assert np.array_equal(ws.iters, np.where(order < n, order, order - n))
+    assert np.array_equal(ws.level_ptr, np.concatenate([[0], np.cumsum(np.bincount(lv)[1:])]))
+
+
+@pytest.mark.parametrize("cfg", (1, 2, 3, 4))
+def test_config_structures_full_size(orc, cfg):
+    M = sf.config_matrix(cfg)
+    combo = CONFIG_COMBO[cfg]
+    st = sf.make_state(combo, M, seed=7)
+    _structures_vs_oracle(orc, st, combo, Csc(M.n, M.colptr, M.rowidx, M.values))
+
+
+@pytest.mark.parametrize("combo", (1, 8))
+def test_config5_structures_full_size(orc, combo):
+    # C5's pattern: 27-point 128^3, 2,097,152 rows, 26.8 M edges per solve DAG
+    M, vals = sf.config5_systems(nsys=1)
+    st = sf.make_state(combo, M, nsys=1, values=vals)
+    _structures_vs_oracle(orc, st, combo, Csc(M.n, M.colptr, M.rowidx, vals))
 
 
 def test_config1_residuals():
