@@ -4,19 +4,26 @@ and HBM GB/s vs the roofline, with the reference CPU executor beside it.
 
 Workload (config.workload): BASELINE config 5, the largest single-GPU
 configuration -- forward L z = b then backward L^T x = z on the 27-point
-128^3 stencil (n = 2,097,152, nnz(L) = 28,920,060), a batch of 8 systems per
-GPU (own diagonal perturbation and right-hand side each), one fused launch
-per step.  One "exec" = one fused kernel-pair execution on one system.
+128^3 stencil (n = 2,097,152, nnz(L) = 28,920,060), BASELINE's batch of 8
+systems (own diagonal perturbation and right-hand side each), one fused
+launch per step.  One "exec" = one fused kernel-pair execution on one system.
 
   python bench.py [--gpus N --steps K --warmup W] [--impl reference]
-  torchrun --nproc-per-node N bench.py --gpus N ...   (one process per GPU)
 
-Multi-GPU: the systems are independent, so each rank runs its own batch of
-8 (weak scaling, no data-path collective); torch.distributed is used only
-for the barrier and the max-over-ranks of the timings.  ``--config 1
---shard-spmv`` runs config 1 with the solve on rank 0 and the SpMV rows
-sharded over the ranks (one point-to-point x exchange + a y all-gather over
-NCCL; strong scaling).
+With --gpus N > 1 and no torchrun environment, bench.py launches its N ranks
+itself (torch.distributed.run, 127.0.0.1); under torchrun WORLD_SIZE must
+equal N.  Multi-GPU: the batch of 8 is sharded, 8/N systems per GPU
+(strong scaling; the systems are independent, so there is no data-path
+collective -- torch.distributed only provides the barrier and the
+max-over-ranks of the timings); ``--systems-per-gpu K`` runs K systems on
+every GPU instead (weak scaling), and at N > 1 the line also carries that
+weak-scaling measurement with K = 8.  ``--config 1 --shard-spmv`` runs
+config 1 with the solve on rank 0 and the SpMV rows sharded over the ranks
+(one point-to-point x exchange + a y all-gather over NCCL; strong scaling).
+
+The reference arm (--impl reference) runs only oracle/_ref (the unmodified
+reference compiled from /root/reference, plus the repo's input generators
+compiled into it) and never imports this package or loads libsfgpu.so.
 """
 from __future__ import annotations
 
@@ -41,7 +48,7 @@ CONFIG_NAME = {
     2: "SpIC0->SpTRSV 3-D 7-pt 64^3 (combo 5)",
     3: "SpILU0->SpTRSV 3-D conv-diff 96^3 (combo 6)",
     4: "DAD->SpIC0 random band n=1e6 (combo 7)",
-    5: "SpTRSV->SpTRSV^T fwd L, bwd L^T, 27-pt 128^3, 8 systems/GPU",
+    5: "SpTRSV->SpTRSV^T fwd L, bwd L^T, 27-pt 128^3, batch of 8 systems",
 }
 
 
@@ -184,11 +191,23 @@ def physical_bytes(cfg: int, n: int, nnzL: int, nnzA: int, S: int) -> int:
     return S * (2 * 8 * nnzL + 4 * 8 * n) + 2 * (4 * nnzL + ptr)
 
 
+def unique_bytes(cfg: int, n: int, nnzL: int, nnzA: int, S: int) -> int:
+    """Algorithmic bytes of one launch with the pattern shared by the S
+    systems counted once (config 5: row pointers and column indices once,
+    values and vectors per system)."""
+    if cfg != 5:
+        return algorithmic_bytes(cfg, n, nnzL, nnzA)
+    return 4 * (n + 1) + 4 * nnzL + S * (8 * nnzL + 3 * 8 * n)
+
+
 def kernel_name(cfg: int, combo: int, S: int) -> str:
+    G = 4 if S <= 8 else 32 // S  # chain_G (csrc/chain.cuh)
+    if cfg == 5 and S == 1:  # 27-point rows: one warp per chain (plan.cu executor choice)
+        return f"k_chain<1,{G},12,{combo}> (fwd L + bwd L^T)"
     if S == 1 and combo in (1, 2, 4, 8):  # single systems: multi-line step-stream executor
         return {4: "k_mline1 (fwd L + SpMV row blocks)", 2: "k_mline1 (SpMV blocks + fwd L)"}.get(
             combo, f"k_mline1 (combo {combo})")
-    return {8: f"k_chain_sm<{S},4,12,8> (fwd L + bwd L^T)", 1: f"k_chain_sm<{S},4,12,1> (fwd L + fwd L)",
+    return {8: f"k_chain_sm<{S},{G},12,8> (fwd L + bwd L^T)", 1: f"k_chain_sm<{S},{G},12,1> (fwd L + fwd L)",
             5: "k_ic0_warp<5>", 6: "k_ilu0_warp<6>", 3: "k_ilu0_warp<3>",
             7: "k_ic0_warp<7>"}.get(combo, f"combo {combo} executor")
 
@@ -248,23 +267,74 @@ def make_inputs(cfg: int, size, nsys: int, sys0: int):
 
 
 # ---------------------------------------------------------------------------
-# the reference CPU executor (oracle/_ref: unmodified reference headers)
+# the reference CPU executor (oracle/_ref: unmodified reference headers).
+# Inputs come from oracle/_ref too (the repo's generators compiled into it),
+# so these legs never load libsfgpu.so.
 # ---------------------------------------------------------------------------
-def reference_fused(cfg: int, M, vals, vin, nthreads: int, warmups: int, repeats: int):
+def ref_inputs(ref, cfg: int, size, nsys: int = 1, sys0: int = 0):
+    if cfg == 5:
+        M, vals = ref.config_matrix(5, size, nsys_perturb=nsys, seed0=1000 + sys0)
+        vin = np.concatenate([ref.gen_vector(M.n, 7 + sys0 + s) for s in range(nsys)])
+        return M, vals, vin
+    M = ref.config_matrix(cfg, size)
+    return M, None, ref.gen_vector(M.n, 7)
+
+
+def reference_fused(cfg: int, M, vin, nthreads: int, warmups: int, repeats: int):
     """Times the reference's execute_fused (msp + compile_schedule once, then
-    warmups + repeats) on one system.  Config 5's fwd->bwd pair does not exist
-    in the reference, so its combo 1 (fwd -> fwd with the same L: identical
-    sizes, bytes and flops) stands in."""
+    warmups + repeats) for configs 1-4 (the reference's own combos)."""
     from oracle.oracle import Csc, Reference
     ref = Reference()
-    combo = 1 if cfg == 5 else CONFIG_COMBO[cfg]
-    v0 = M.values if vals is None else vals[:M.nnz]
-    st = ref.state(combo, Csc(M.n, M.colptr, M.rowidx, v0), 7, vin=vin[:M.n])
+    combo = CONFIG_COMBO[cfg]
+    st = ref.state(combo, Csc(M.n, M.colptr, M.rowidx, M.values), 7, vin=vin[:M.n])
     t0 = time.perf_counter()
     times, insp, nsp = st.bench(1, nthreads, warmups, repeats)
     wall = time.perf_counter() - t0
     return {"times": times.tolist(), "median_s": float(np.median(times)), "inspector_s": insp,
             "s_partitions": nsp, "combo": combo, "wall_s": wall}
+
+
+class RefConfig5:
+    """Config 5 (fwd L z = b, then bwd L^T x = z) on the reference's own
+    parallel executor.  The reference has no backward solve and no such
+    pair, so each system's two solves run as single kernels -- kernel 1 of a
+    combo-1 KernelState under its LBC schedule, executed by execute_unfused
+    (executor.hpp:325-381) with an empty kernel-2 schedule -- the backward
+    one on permute_symmetric(transpose(L), rev) (matrix.hpp:130-173) with z
+    reversed, exactly SURVEY.md 8(c)'s composition.  The systems share the
+    pattern, so the DAG and LBC schedule are built once per direction and
+    each system's state differs only on its diagonal.  A step's time is the
+    sum of the executor wall times (ExecStats::wall_ns) of its solves."""
+
+    def __init__(self, ref, M, vals, vin, nsys: int, nthreads: int):
+        from oracle.oracle import Csc
+        self.n, self.nsys, self.vin = M.n, nsys, vin
+        n = M.n
+        cols = np.repeat(np.arange(n, dtype=np.int64), np.diff(M.colptr))
+        dpos = np.nonzero(M.rowidx == cols)[0]
+        t0 = time.perf_counter()
+        M0 = Csc(n, M.colptr, M.rowidx, vals[:M.nnz])
+        f0 = ref.solver(M0, nthreads)
+        b0 = ref.solver(ref.backward_matrix(M0), nthreads)
+        self.inspector_s = f0.inspector_s + b0.inspector_s
+        self.fwd, self.bwd = [f0], [b0]
+        for s in range(1, nsys):
+            d = vals[s * M.nnz:(s + 1) * M.nnz][dpos]
+            self.fwd.append(f0.with_diagonal(d))
+            self.bwd.append(b0.with_diagonal(d[::-1].copy()))
+        self.setup_s = time.perf_counter() - t0
+        self.z = np.empty(n)
+        self.xr = np.empty(n)
+
+    def step(self, out=None) -> float:
+        n, secs = self.n, 0.0
+        for s in range(self.nsys):
+            secs += self.fwd[s].run(self.vin[s * n:(s + 1) * n], self.z)
+            secs += self.bwd[s].run(self.z[::-1].copy(), self.xr)
+            if out is not None:
+                out[s, :n] = self.z
+                out[s, n:] = self.xr[::-1]
+        return secs
 
 
 def cpu_threads() -> int:
@@ -277,13 +347,44 @@ def cpu_threads() -> int:
 # ---------------------------------------------------------------------------
 # our arm
 # ---------------------------------------------------------------------------
+GLOBAL_BATCH = 8  # BASELINE.json configs[4]: a batch of 8 independent systems
+
+
+def systems_per_gpu(args, D) -> int:
+    """Config 5: BASELINE's batch of 8 sharded over the ranks (8/N each), or
+    --systems-per-gpu K on every rank (weak scaling)."""
+    if args.systems_per_gpu is not None:
+        return args.systems_per_gpu
+    if GLOBAL_BATCH % D.world:
+        raise SystemExit(f"the batch of {GLOBAL_BATCH} does not split over {D.world} GPUs; "
+                         "pass --systems-per-gpu")
+    return GLOBAL_BATCH // D.world
+
+
+def scaling_kind(args, cfg, D) -> str:
+    return "weak" if (cfg == 5 and args.systems_per_gpu is not None) else "strong"
+
+
+def check_result(st, cfg, combo, M, vals, vin, S):
+    """Bit-exact check of the plan's last execution (system 0) against the
+    oracle -- the result the timed loop produced."""
+    from oracle.oracle import Csc, Oracle
+    orc = Oracle()
+    n = M.n
+    v0 = M.values if vals is None else vals[:M.nnz]
+    want = orc.run_sequential(combo, Csc(n, M.colptr, M.rowidx, v0), 7, vin=vin[:n])
+    got = st.collect_outputs()[:len(want)]
+    return {"checked": "system 0 of this rank's batch vs oracle/sf_oracle.c",
+            "bit_exact": bool(np.array_equal(got, want))}
+
+
 def run_ours(args, D: Dist):
     import paper_2111_12238_b200 as sf
     from paper_2111_12238_b200 import abi
     abi.set_device(D.local)
     cfg = args.config
     combo = CONFIG_COMBO[cfg] if not (cfg == 5 and args.mode == "fwdfwd") else 1
-    S = args.systems_per_gpu if cfg == 5 else 1
+    S = systems_per_gpu(args, D) if cfg == 5 else 1
     t0 = time.perf_counter()
     M, vals, vin = make_inputs(cfg, args.size, S, D.rank * S)
     t_gen = time.perf_counter() - t0
@@ -315,6 +416,15 @@ def run_ours(args, D: Dist):
     u_total, u_kernel = st.bench(args.steps, unfused=True)
     D.barrier()
     u_ms = D.max(u_total / args.steps)
+
+    # ---- the joint-DAG wavefront executor (execute_joint_wavefront, the
+    # paper's level-set baseline) on the same inputs
+    st.bench(max(1, args.warmup), unfused=2)
+    D.barrier()
+    w_total, w_kernel = st.bench(args.steps, unfused=2)
+    D.barrier()
+    w_ms = D.max(w_total / args.steps)
+    w_levels = int(st.wavefront().nlevels())
 
     # ---- end to end through the public API: H2D of the step's inputs, the
     # execution, D2H of the step's outputs.  Solve pairs go through
@@ -372,14 +482,17 @@ def run_ours(args, D: Dist):
         cb["frac_of_step"] = cb["both_ms"] / (e2e_s * 1e3)
     e2e["copy_floor"] = cb
 
-    # ---- check the timed result once more against the oracle (rank 0, small cost)
+    # ---- the timed execution's result against the oracle (system 0 of the
+    # rank; the plan's outputs are those of its last execution)
+    parity = check_result(st, cfg, combo, M, vals, vin, S)
     peak, peak_src = hbm_peak()
     achieved = bytes_per_launch / (kernel_ms / 1e3) / 1e9
     workload = f"config{cfg}"
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": D.world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "scaling": scaling_kind(args, cfg, D), "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
         "config": {"workload": CONFIG_NAME[cfg] if not (cfg == 5 and combo == 1)
                    else CONFIG_NAME[5].replace("bwd L^T", "fwd L (combo 1 parity mode)"),
                    "baseline_config": cfg, "combo": combo, "n": M.n, "nnz_A": M.nnz,
@@ -387,6 +500,7 @@ def run_ours(args, D: Dist):
                    "l2": "inputs larger than L2 (L values+indices %.2f GB/GPU > 126 MB)"
                    % (S * 12 * nnzL / 1e9) if cfg == 5 else "see DESIGN.md",
                    "parallelism": f"dp{D.world} (independent systems, no collective)"},
+        "parity": parity,
         "gpu_launches": launches,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": ncu_traffic(workload),
@@ -395,9 +509,16 @@ def run_ours(args, D: Dist):
                      "kernel": kernel_name(cfg, combo, S),
                      "physical_bytes_per_launch": physical_bytes(cfg, M.n, nnzL, M.nnz, S),
                      "physical_frac": physical_bytes(cfg, M.n, nnzL, M.nnz, S)
+                     / (kernel_ms / 1e3) / 1e9 / peak,
+                     # the shared pattern counted once instead of once per system
+                     "unique_bytes_per_launch": unique_bytes(cfg, M.n, nnzL, M.nnz, S),
+                     "unique_frac": unique_bytes(cfg, M.n, nnzL, M.nnz, S)
                      / (kernel_ms / 1e3) / 1e9 / peak},
         "unfused": {"ms_per_step": u_ms, "value": S * D.world / (u_ms / 1e3),
                     "fused_speedup": u_ms / ms_step},
+        "wavefront": {"ms_per_step": w_ms, "value": S * D.world / (w_ms / 1e3),
+                      "levels": w_levels, "fused_speedup": w_ms / ms_step,
+                      "executor": "joint-DAG level sets, grid barrier per level (sfg_execute_wavefront)"},
         "e2e": e2e,
         "clocks": clk.summary(),
         "clocks_e2e": clk_e2e.summary(),
@@ -406,7 +527,21 @@ def run_ours(args, D: Dist):
 
     # ---- CPU baseline: the reference's fused executor on the box's host cores
     if D.world == 1 and D.rank == 0 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline(cfg, M, vals, vin)
+        line["cpu_baseline"] = cpu_baseline(cfg, args.size)
+
+    # ---- weak scaling beside the sharded batch: 8 systems on every GPU
+    if D.world > 1 and cfg == 5 and args.systems_per_gpu is None and not args.no_extras:
+        Mw, valsw, vinw = make_inputs(5, args.size, GLOBAL_BATCH, D.rank * GLOBAL_BATCH)
+        sw = sf.make_state(8, Mw, seed=7, nsys=GLOBAL_BATCH, values=valsw, vin=vinw).inspect()
+        sw.bench(args.warmup)
+        D.barrier()
+        wt, _ = sw.bench(args.steps)
+        D.barrier()
+        wms = D.max(wt / args.steps)
+        line["weak_scaling"] = {"systems_per_gpu": GLOBAL_BATCH, "global_systems": GLOBAL_BATCH * D.world,
+                                "ms_per_step": wms, "value": GLOBAL_BATCH * D.world / (wms / 1e3),
+                                "scaling": "weak"}
+        sw.close()
 
     # ---- the other BASELINE configs on this GPU (single GPU only)
     if D.world == 1 and not args.no_extras and cfg == 5:
@@ -507,27 +642,40 @@ def run_sharded(args, D: Dist):
     }
 
 
-def cpu_baseline(cfg, M, vals, vin):
+def cpu_baseline(cfg, size):
+    """The reference on this box's host cores, a bounded sample of the
+    workload (inputs generated by oracle/_ref, not by this package)."""
     from oracle.oracle import Reference
     T = cpu_threads()
-    if Reference.available():
-        r = reference_fused(cfg, M, vals, vin, T, warmups=1, repeats=3)
-        sample = ("1 system of the batch, reference execute_fused (msp + compile_schedule, "
-                  f"T={T}), median of {len(r['times'])} after 1 warm-up")
-        if cfg == 5:
-            sample += ("; combo 1 fwd->fwd on the same L (the reference has no backward "
-                       "L^T solve)")
-        return {"value": 1.0 / r["median_s"], "unit": UNIT, "cores": T, "kind": "reference",
-                "sample": sample, "ms_per_exec": r["median_s"] * 1e3,
-                "inspector_s": r["inspector_s"], "s_partitions": r["s_partitions"]}
-    from oracle.oracle import Csc, Oracle
-    orc = Oracle()
-    v0 = M.values if vals is None else vals[:M.nnz]
-    t0 = time.perf_counter()
-    orc.run_sequential(CONFIG_COMBO[cfg], Csc(M.n, M.colptr, M.rowidx, v0), 7, vin=vin[:M.n])
-    dt = time.perf_counter() - t0
-    return {"value": 1.0 / dt, "unit": UNIT, "cores": 1, "kind": "port",
-            "sample": "1 system, oracle sequential restatement (make_state included)"}
+    if not Reference.available():
+        from oracle.oracle import Csc, Oracle
+        import paper_2111_12238_b200 as sf
+        M = sf.config_matrix(cfg, size=size) if cfg != 5 else sf.config5_systems(size=size, nsys=1)[0]
+        orc = Oracle()
+        t0 = time.perf_counter()
+        orc.run_sequential(CONFIG_COMBO[cfg], Csc(M.n, M.colptr, M.rowidx, M.values), 7)
+        dt = time.perf_counter() - t0
+        return {"value": 1.0 / dt, "unit": UNIT, "cores": 1, "kind": "port",
+                "sample": "1 system, oracle sequential restatement (make_state included)"}
+    ref = Reference()
+    if cfg == 5:
+        M, vals, vin = ref_inputs(ref, 5, size, 1, 0)
+        r = RefConfig5(ref, M, vals, vin, 1, T)
+        r.step()  # warm-up
+        times = [r.step() for _ in range(3)]
+        med = float(np.median(times))
+        return {"value": 1.0 / med, "unit": UNIT, "cores": T, "kind": "reference",
+                "sample": ("1 system of the batch (fwd L then bwd L^T on the reference's "
+                           f"parallel executor, T={T}, LBC schedules built once), median of 3 "
+                           "after 1 warm-up"),
+                "ms_per_exec": med * 1e3, "inspector_s": r.inspector_s}
+    M, _, vin = ref_inputs(ref, cfg, size)
+    r = reference_fused(cfg, M, vin, T, warmups=1, repeats=3)
+    return {"value": 1.0 / r["median_s"], "unit": UNIT, "cores": T, "kind": "reference",
+            "sample": (f"reference execute_fused (msp + compile_schedule, T={T}), median of "
+                       f"{len(r['times'])} after 1 warm-up"),
+            "ms_per_exec": r["median_s"] * 1e3, "inspector_s": r["inspector_s"],
+            "s_partitions": r["s_partitions"]}
 
 
 def other_configs(args):
@@ -544,6 +692,8 @@ def other_configs(args):
         st.bench(3)
         tot, ker = st.bench(reps)
         ut, uk = st.bench(reps, unfused=True)
+        st.bench(2, unfused=2)
+        wt, wk = st.bench(reps, unfused=2)
         nnzL = lower_nnz(M)
         byts = algorithmic_bytes(cfg, M.n, nnzL, M.nnz)
         ms = tot / reps
@@ -552,6 +702,7 @@ def other_configs(args):
                "achieved_gbs": byts / (ker / 1e3) / 1e9,
                "frac": byts / (ker / 1e3) / 1e9 / peak,
                "unfused_ms_per_exec": ut / reps, "fused_speedup": (ut / reps) / ms,
+               "wavefront_ms_per_exec": wt / reps, "speedup_vs_wavefront": (wt / reps) / ms,
                # level_info(joint_dag) (dag.hpp:197-218) and the executor's own
                # dependency levels (s-partitions of its FusedPartitioning)
                "critical_path": int(st.level_info(3).critical_path),
@@ -559,7 +710,7 @@ def other_configs(args):
                "traffic": ncu_traffic(f"config{cfg}")}
         if Reference.available() and not args.no_cpu_baseline:
             try:
-                r = reference_fused(cfg, M, None, vin, T, warmups=1, repeats=3)
+                r = reference_fused(cfg, M, vin, T, warmups=1, repeats=3)
                 rec["cpu_reference"] = {"value": 1.0 / r["median_s"], "cores": T,
                                         "ms_per_exec": r["median_s"] * 1e3,
                                         "inspector_s": r["inspector_s"]}
@@ -580,7 +731,7 @@ def other_configs(args):
     # config 5's systems under the reference's own combo 1 (fwd L -> fwd L, the
     # pair the CPU baseline times): its joint DAG lets the second solve trail
     # the first, so fused should beat the unfused two-launch sequence
-    S = args.systems_per_gpu
+    S = args.systems_per_gpu or GLOBAL_BATCH
     M, vals, vin = make_inputs(5, args.size, S, 0)
     st = sf.make_state(1, M, seed=7, nsys=S, values=vals, vin=vin).inspect()
     reps = 20
@@ -624,27 +775,47 @@ def run_reference(args, D: Dist):
     cfg = args.config
     if not Reference.available():
         return {"impl": "reference", "unavailable": "oracle/_ref/libsfref.so not built"}
-    M, vals, vin = make_inputs(cfg, args.size, 1, 0)
+    ref = Reference()
     T = cpu_threads()
-    r = reference_fused(cfg, M, vals, vin, T, warmups=max(args.warmup, 1), repeats=args.steps)
-    mean_s = float(np.mean(r["times"]))
-    value = 1.0 / mean_s
-    sample = (f"reference execute_fused, T={T} host threads, 1 system per step "
-              f"({args.steps} steps after {max(args.warmup, 1)} warm-ups; msp inspector "
-              f"{r['inspector_s']:.1f}s excluded)")
+    warm = max(args.warmup, 1)
     if cfg == 5:
-        sample += "; combo 1 fwd->fwd on the same L (no backward L^T solve in the reference)"
+        # BASELINE's whole batch of 8 every step, like our arm's global batch
+        nsys = 8 if args.systems_per_gpu is None else args.systems_per_gpu * D.world
+        M, vals, vin = ref_inputs(ref, 5, args.size, nsys, 0)
+        r = RefConfig5(ref, M, vals, vin, nsys, T)
+        for _ in range(warm):
+            r.step()
+        times = [r.step() for _ in range(args.steps)]
+        mean_s = float(np.mean(times))
+        value = nsys / mean_s
+        combo, insp, nsp = 8, r.inspector_s, None
+        sample = (f"the whole batch of {nsys} systems per step, each a fwd L then bwd L^T solve "
+                  f"on the reference's parallel executor (execute_unfused, LBC schedules, T={T}; "
+                  "the reference has no fwd->bwd pair), sum of executor wall times; "
+                  f"{args.steps} steps after {warm} warm-ups; schedules built once "
+                  f"({insp:.1f}s, excluded)")
+        cfgd = {"workload": CONFIG_NAME[5], "baseline_config": 5, "combo": 8, "n": M.n,
+                "nnz_A": M.nnz, "global_systems": nsys}
+    else:
+        M, _, vin = ref_inputs(ref, cfg, args.size)
+        r = reference_fused(cfg, M, vin, T, warmups=warm, repeats=args.steps)
+        mean_s = float(np.mean(r["times"]))
+        value = 1.0 / mean_s
+        combo, insp, nsp = r["combo"], r["inspector_s"], r["s_partitions"]
+        sample = (f"reference execute_fused, T={T} host threads, 1 execution per step "
+                  f"({args.steps} steps after {warm} warm-ups; msp inspector {insp:.1f}s excluded)")
+        cfgd = {"workload": CONFIG_NAME[cfg], "baseline_config": cfg, "combo": combo, "n": M.n,
+                "nnz_A": M.nnz, "global_systems": 1}
+    assert "paper_2111_12238_b200" not in sys.modules, "the reference arm must not load our package"
     return {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": D.world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": mean_s * 1e3,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic",
-        "config": {"workload": CONFIG_NAME[cfg], "baseline_config": cfg, "combo": r["combo"],
-                   "n": M.n, "nnz_A": M.nnz, "systems_per_step": 1},
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": cfgd,
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": T, "kind": "reference",
                          "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        "inspector_s": r["inspector_s"], "s_partitions": r["s_partitions"],
+        "inspector_s": insp, "s_partitions": nsp, "package_loaded": False,
     }
 
 
@@ -665,6 +836,21 @@ class _Solo(Dist):
         pass
 
 
+def spawn_ranks(n: int) -> int:
+    """--gpus N without a torchrun environment: launch the N ranks here
+    (torch.distributed.run on 127.0.0.1, one process per GPU).  Rank 0
+    prints the JSON line."""
+    import socket
+    import subprocess
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port),
+           os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -673,7 +859,9 @@ def main():
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--config", type=int, default=5, choices=(1, 2, 3, 4, 5))
     ap.add_argument("--mode", choices=("fwdbwd", "fwdfwd"), default="fwdbwd")
-    ap.add_argument("--systems-per-gpu", type=int, default=8)
+    ap.add_argument("--systems-per-gpu", type=int, default=None,
+                    help="config 5: systems on every GPU (weak scaling); default: the batch "
+                         "of 8 split over the GPUs")
     ap.add_argument("--size", type=int, default=None, help="grid side / n override (testing)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-extras", action="store_true")
@@ -682,6 +870,10 @@ def main():
     args = ap.parse_args()
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        sys.exit(spawn_ranks(args.gpus))
+    if "WORLD_SIZE" in os.environ and int(os.environ["WORLD_SIZE"]) != args.gpus:
+        ap.error(f"--gpus {args.gpus} but WORLD_SIZE={os.environ['WORLD_SIZE']}")
     if args.impl == "reference" and int(os.environ.get("RANK", "0")) != 0:
         return  # the reference arm runs on rank 0 only
     D = Dist() if args.impl == "ours" else _Solo()

@@ -296,6 +296,23 @@ class Reference:
         L.ref_validate_partitioning.restype = C.c_int64
         L.ref_read_mm.argtypes = [C.c_char_p, C.c_char_p, C.c_int]
         L.ref_read_mm.restype = vp
+        L.ref_fwd_bwd.argtypes = [C.c_int32, _i32p, _i32p, _f64p, _f64p, _f64p, _i32p,
+                                  C.c_char_p, C.c_int]
+        L.ref_backward_matrix.argtypes = [C.c_int32, _i32p, _i32p, _f64p]
+        L.ref_backward_matrix.restype = vp
+        L.ref_solver_new.argtypes = [C.c_int32, _i32p, _i32p, _f64p, C.c_int32, _f64p]
+        L.ref_solver_new.restype = vp
+        L.ref_solver_run.argtypes = [vp, _f64p, _f64p, _f64p, _i32p, C.c_char_p, C.c_int]
+        L.ref_solver_free.argtypes = [vp]
+        L.ref_solver_clone_diag.argtypes = [vp, _f64p]
+        L.ref_solver_clone_diag.restype = vp
+        # the repo's BASELINE generators (fixtures.cpp compiled in, renamed)
+        L.refgen_matrix_gen.argtypes = [C.c_int32, C.c_int32, C.c_int32, C.c_uint64,
+                                        C.POINTER(vp)]
+        L.refgen_matrix_dims.argtypes = [vp, _i32p, _i64p]
+        L.refgen_matrix_copy.argtypes = [vp, _i32p, _i32p, _f64p]
+        L.refgen_matrix_free.argtypes = [vp]
+        L.refgen_matrix_perturb_diag.argtypes = [vp, C.c_int32, C.c_uint64, _f64p]
         self.lib = L
 
     # ---- fixtures.hpp
@@ -317,6 +334,69 @@ class Reference:
         self.lib.ref_mat_copy(h, _p(cp, _i32p), _p(ri, _i32p), _p(va, _f64p))
         self.lib.ref_mat_free(h)
         return Csc(n.value, cp, ri[:nnz.value], va[:nnz.value])
+
+    # ---- BASELINE.json configurations (the repo's generators, not libsfgpu)
+    FULL_SIZE = {1: 512, 2: 64, 3: 96, 4: 1_000_000, 5: 128}
+
+    def config_matrix(self, cfg: int, size: int | None = None, seed: int = 7,
+                      halfwidth: int = 2000, nsys_perturb: int = 0, seed0: int = 1000):
+        """The same inputs as paper_2111_12238_b200.config_matrix /
+        config5_systems, generated by fixtures.cpp compiled into libsfref.so."""
+        a = size or self.FULL_SIZE[cfg]
+        b = halfwidth if cfg == 4 else 0
+        h = C.c_void_p()
+        if self.lib.refgen_matrix_gen(9 + cfg, a, b, seed, C.byref(h)) != 0:
+            raise ValueError("bad generator parameters")
+        try:
+            n = C.c_int32()
+            nnz = C.c_int64()
+            self.lib.refgen_matrix_dims(h, C.byref(n), C.byref(nnz))
+            cp = np.empty(n.value + 1, np.int32)
+            ri = np.empty(max(nnz.value, 1), np.int32)
+            va = np.empty(max(nnz.value, 1), np.float64)
+            self.lib.refgen_matrix_copy(h, _p(cp, _i32p), _p(ri, _i32p), _p(va, _f64p))
+            M = Csc(n.value, cp, ri[:nnz.value], va[:nnz.value])
+            if nsys_perturb:
+                vals = np.empty(nsys_perturb * nnz.value, np.float64)
+                self.lib.refgen_matrix_perturb_diag(h, nsys_perturb, seed0, _p(vals, _f64p))
+                return M, vals
+            return M
+        finally:
+            self.lib.refgen_matrix_free(h)
+
+    def fwd_bwd(self, M: Csc, b: np.ndarray) -> np.ndarray:
+        """Config 5's pair from the reference's primitives:
+        z = sptrsv(L, b); x from sptrsv on permute_symmetric(transpose(L), rev).
+        Returns z ++ x."""
+        out = np.empty(2 * M.n, np.float64)
+        ei = C.c_int32(-1)
+        msg = C.create_string_buffer(256)
+        b = np.ascontiguousarray(b, np.float64)
+        rc = self.lib.ref_fwd_bwd(M.n, _p(M.colptr, _i32p), _p(M.rowidx, _i32p),
+                                  _p(M.values, _f64p), _p(b, _f64p), _p(out, _f64p),
+                                  C.byref(ei), msg, 256)
+        if rc:
+            raise RuntimeError(msg.value.decode())
+        return out
+
+    def backward_matrix(self, M: Csc) -> Csc:
+        """permute_symmetric(transpose(lower_triangle(M)), rev)."""
+        h = self.lib.ref_backward_matrix(M.n, _p(M.colptr, _i32p), _p(M.rowidx, _i32p),
+                                         _p(M.values, _f64p))
+        if not h:
+            raise ValueError("backward_matrix failed")
+        n = C.c_int32()
+        nnz = C.c_int32()
+        self.lib.ref_mat_dims(h, C.byref(n), C.byref(nnz))
+        cp = np.empty(n.value + 1, np.int32)
+        ri = np.empty(max(nnz.value, 1), np.int32)
+        va = np.empty(max(nnz.value, 1), np.float64)
+        self.lib.ref_mat_copy(h, _p(cp, _i32p), _p(ri, _i32p), _p(va, _f64p))
+        self.lib.ref_mat_free(h)
+        return Csc(n.value, cp, ri[:nnz.value], va[:nnz.value])
+
+    def solver(self, M: Csc, nthreads: int) -> "RefSolver":
+        return RefSolver(self, M, nthreads)
 
     def read_matrix_market(self, path: str) -> Csc:
         """The reference's read_matrix_market (matrix_market.hpp:59-121).
@@ -423,6 +503,50 @@ class Reference:
             return Levels(lv[:n], ht[:n], sl[:n], P.value)
         finally:
             self.lib.ref_dag_free(h)
+
+
+class RefSolver:
+    """L x = b with the reference's own parallel executor (kernel 1 of a
+    combo-1 state under its LBC schedule, execute_unfused with an empty
+    kernel-2 schedule; the schedule is built once)."""
+
+    def __init__(self, ref: "Reference", M: Csc | None, nthreads: int, _handle=None):
+        self.ref = ref
+        if _handle is not None:
+            self.h, self.n, self.inspector_s = _handle
+            return
+        self.n = M.n
+        insp = C.c_double()
+        self.h = ref.lib.ref_solver_new(M.n, _p(M.colptr, _i32p), _p(M.rowidx, _i32p),
+                                        _p(M.values, _f64p), nthreads, C.byref(insp))
+        if not self.h:
+            raise RuntimeError("ref_solver_new failed")
+        self.inspector_s = insp.value
+
+    def with_diagonal(self, diag: np.ndarray) -> "RefSolver":
+        """The same pattern and schedule, row i's diagonal set to diag[i]."""
+        diag = np.ascontiguousarray(diag, np.float64)
+        h = self.ref.lib.ref_solver_clone_diag(self.h, _p(diag, _f64p))
+        if not h:
+            raise RuntimeError("ref_solver_clone_diag failed")
+        return RefSolver(self.ref, None, 0, _handle=(h, self.n, 0.0))
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            self.ref.lib.ref_solver_free(self.h)
+            self.h = None
+
+    def run(self, b: np.ndarray, x: np.ndarray | None = None) -> float:
+        """x = L^-1 b; returns the executor's wall seconds."""
+        b = np.ascontiguousarray(b, np.float64)
+        wall = C.c_double()
+        ei = C.c_int32(-1)
+        msg = C.create_string_buffer(256)
+        rc = self.ref.lib.ref_solver_run(self.h, _p(b, _f64p), _p(x, _f64p) if x is not None else None,
+                                         C.byref(wall), C.byref(ei), msg, 256)
+        if rc:
+            raise RuntimeError(msg.value.decode())
+        return wall.value
 
 
 class RefState:

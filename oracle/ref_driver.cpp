@@ -8,6 +8,12 @@
 // functions.  Used (a) to pin the C restatement in oracle/sf_oracle.c,
 // (b) to generate tests/golden/ fixtures, and (c) as the CPU baseline
 // ("kind": "reference") timed by bench.py.
+//
+// The BASELINE.json input generators are this repository's own
+// (paper_2111_12238_b200/csrc/fixtures.cpp); oracle/Makefile compiles that
+// file into this library under renamed symbols (sfg_* -> refgen_*), so the
+// reference arm of bench.py generates its inputs without loading
+// libsfgpu.so.
 #include <sparsefuse/dag.hpp>
 #include <sparsefuse/executor.hpp>
 #include <sparsefuse/fixtures.hpp>
@@ -391,6 +397,110 @@ void* ref_read_mm(const char* path, char* msg, int ml) {
     return new CscMatrix(read_matrix_market(path));
   } catch (const std::exception& e) {
     put_msg(msg, ml, e.what());
+    return nullptr;
+  }
+}
+
+// ---- config 5 (forward L then backward L^T) from the reference's primitives
+// (the reference has no backward solve):
+//   z = sptrsv(to_csr(lower_triangle(M)), b)                 kernels.hpp:335-342
+//   B = permute_symmetric(transpose(lower_triangle(M)), rev) matrix.hpp:130-173
+//   x'= sptrsv(to_csr(B), z'),  z'[n-1-i] = z[i],  x[i] = x'[n-1-i]
+// out = z ++ x (collect_outputs layout of a solve pair).
+int ref_fwd_bwd(int32_t n, const int32_t* colptr, const int32_t* rowidx, const double* values,
+                const double* b, double* out, int32_t* err_index, char* msg, int ml) {
+  return guarded(
+      [&] {
+        const CscMatrix L = lower_triangle(from_arrays(n, colptr, rowidx, values));
+        const DenseVector z = sptrsv(to_csr(L), DenseVector(b, b + n));
+        std::vector<Index> rev((size_t)n);
+        for (Index i = 0; i < n; ++i)
+          rev[(size_t)i] = n - 1 - i;
+        const CscMatrix B = permute_symmetric(transpose(L), rev);
+        DenseVector zr((size_t)n);
+        for (Index i = 0; i < n; ++i)
+          zr[(size_t)(n - 1 - i)] = z[(size_t)i];
+        const DenseVector xr = sptrsv(to_csr(B), zr);
+        for (Index i = 0; i < n; ++i) {
+          out[i] = z[(size_t)i];
+          out[n + i] = xr[(size_t)(n - 1 - i)];
+        }
+      },
+      err_index, msg, ml);
+}
+
+// B = permute_symmetric(transpose(lower_triangle(M)), rev) as a matrix handle
+void* ref_backward_matrix(int32_t n, const int32_t* colptr, const int32_t* rowidx,
+                          const double* values) {
+  try {
+    const CscMatrix L = lower_triangle(from_arrays(n, colptr, rowidx, values));
+    std::vector<Index> rev((size_t)n);
+    for (Index i = 0; i < n; ++i)
+      rev[(size_t)i] = n - 1 - i;
+    return new CscMatrix(permute_symmetric(transpose(L), rev));
+  } catch (...) {
+    return nullptr;
+  }
+}
+
+// One triangular solve L x = b on the reference's own parallel executor:
+// kernel 1 of a combo-1 KernelState under its LBC schedule
+// (build_kernel_schedule, executor.hpp:158-202) run by execute_unfused
+// (executor.hpp:325-381) with an empty kernel-2 schedule.  The schedule is
+// built once (the inspector); each run sets vin and returns x.
+struct RefSolver {
+  KernelState st;
+  UnfusedSchedule us;
+  Index nthreads = 1;
+};
+
+void* ref_solver_new(int32_t n, const int32_t* colptr, const int32_t* rowidx,
+                     const double* values, int32_t nthreads, double* inspector_s) {
+  try {
+    auto* s = new RefSolver();
+    s->st = make_state(1, from_arrays(n, colptr, rowidx, values), 7);
+    s->nthreads = nthreads;
+    const double t0 = now_s();
+    s->us.k1 = build_kernel_schedule(build_g1(s->st), nthreads);
+    if (inspector_s)
+      *inspector_s = now_s() - t0;
+    return s;
+  } catch (...) {
+    return nullptr;
+  }
+}
+
+// runs the solve; *wall_s = ExecStats::wall_ns (the parallel region)
+int ref_solver_run(void* h, const double* b, double* x, double* wall_s, int32_t* err_index,
+                   char* msg, int ml) {
+  auto* s = static_cast<RefSolver*>(h);
+  return guarded(
+      [&] {
+        std::copy(b, b + s->st.n, s->st.vin.begin());
+        const ExecStats es = execute_unfused(s->us, s->st, s->nthreads);
+        if (wall_s)
+          *wall_s = (double)es.wall_ns * 1e-9;
+        if (x)
+          std::copy(s->st.vmid.begin(), s->st.vmid.end(), x);
+      },
+      err_index, msg, ml);
+}
+
+void ref_solver_free(void* h) { delete static_cast<RefSolver*>(h); }
+
+// A solver for the same pattern whose matrix differs only on the diagonal
+// (config 5's systems: L_s = L + diag(delta_s)): copies the template's state
+// and schedule, then sets row i's diagonal (stored last, trsv_csr_row) to
+// diag[i].  Saves rebuilding the same DAG and LBC schedule per system.
+void* ref_solver_clone_diag(void* h, const double* diag) {
+  try {
+    const auto* t = static_cast<RefSolver*>(h);
+    auto* s = new RefSolver(*t);
+    CsrMatrix& L = s->st.L_csr;
+    for (Index i = 0; i < L.nrows; ++i)
+      L.values[(size_t)L.rowptr[(size_t)i + 1] - 1] = diag[i];
+    return s;
+  } catch (...) {
     return nullptr;
   }
 }

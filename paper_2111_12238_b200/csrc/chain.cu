@@ -909,20 +909,30 @@ template <int S, int G, int COMBO> void launch_g(const ChainArgs& a, cudaStream_
   SFG_CUDA(cudaGetLastError());
 }
 
-// Tile height G (rows in flight per chain): 32/S capped at 8 by default;
-// a.tile_rows overrides it for single-system plans (G in {1, 2, 4, 8}).
+// Tile height G (rows in flight per chain): chain_G (chain.cuh); a.tile_rows
+// (a power of two with G * S <= 32) overrides it.
 template <int S, int COMBO> void launch_t(const ChainArgs& a, cudaStream_t s) {
-  constexpr int G = 32 / S < 8 ? 32 / S : 8;
-  if (S == 1 && a.tile_rows > 0 && a.tile_rows != G) {
+  constexpr int G = S <= 8 ? 4 : 32 / S; // chain_G's default (chain.cuh)
+  if (a.tile_rows > 0 && a.tile_rows != G && a.tile_rows * S <= 32) {
     switch (a.tile_rows) {
     case 1:
       launch_g<S, 1, COMBO>(a, s);
       return;
     case 2:
-      launch_g<S, 2, COMBO>(a, s);
+      if constexpr (2 * S <= 32)
+        launch_g<S, 2, COMBO>(a, s);
       return;
     case 4:
-      launch_g<S, 4, COMBO>(a, s);
+      if constexpr (4 * S <= 32)
+        launch_g<S, 4, COMBO>(a, s);
+      return;
+    case 8:
+      if constexpr (8 * S <= 32)
+        launch_g<S, 8, COMBO>(a, s);
+      return;
+    case 16:
+      if constexpr (16 * S <= 32 && S >= 2)
+        launch_g<S, 16, COMBO>(a, s);
       return;
     default:
       break;

@@ -76,7 +76,7 @@ struct ChainArgs {
   double* vmid = nullptr;
   double* vout = nullptr;
   int blocks_per_sm = 0;
-  int tile_rows = 0; // single-system tile height override (0 = default)
+  int tile_rows = 0; // tile height override (0 = chain_G's default)
   unsigned bwd_gate = 500; // ns a backward chain's first lane sleeps per check (0 = off)
   // optional timeline trace: per (work item, tile) {claim, partial done,
   // carry done} in %globaltimer ns (diagnostics only; null in production)
@@ -86,9 +86,15 @@ struct ChainArgs {
 
 // Tile geometry for S interleaved systems: G rows in flight per chain (one
 // chain per warp).
+// Tile height: 4 rows for S <= 8 systems, 32/S above.  Measured on C5
+// (config 5's 27-point 128^3 fwd->bwd, ms per launch for S = 1 / 2 / 4 / 8):
+// G = 2: 3.11 / 2.41 / 2.31 / 2.38; G = 4: 2.71 / 2.16 / 2.07 / 1.94;
+// G = 8: 3.56 / 3.15 / 2.89 / -; G = 16: - / 5.40 / - / -.  Longer tiles
+// lengthen the lag per chain level (paid at every one of the 382 levels),
+// shorter ones the per-tile overhead; idle lanes at S < 8 cost little.
 inline int32_t chain_G(int32_t S, int32_t override_rows = 0) {
-  const int32_t g = 32 / S < 8 ? 32 / S : 8;
-  return (S == 1 || S == 8) && override_rows > 0 && override_rows <= g ? override_rows : g;
+  const int32_t g = S <= 8 ? 4 : 32 / S;
+  return override_rows > 0 && override_rows * S <= 32 ? override_rows : g;
 }
 inline int32_t chain_CS(int32_t) { return 1; }
 

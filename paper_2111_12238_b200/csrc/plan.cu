@@ -82,7 +82,7 @@ struct sfg_plan {
   int32_t ell_chn = 0;
   DBuf<int32_t> tail_ptr, tail_rows;
   std::vector<int32_t> row_maxcol; // (unused by the chain path; kept for stats)
-  int32_t tile_rows = 0;           // chain tile height override (S == 1)
+  int32_t tile_rows = 0;           // chain tile height override (0 = chain_G default)
   DBuf<unsigned long long> trace;  // SFG_TRACE diagnostics
   // multi-chain warp executor (combos 1, 8; default)
   bool use_mline = false;
@@ -731,8 +731,14 @@ void do_inspect(sfg_plan* P) {
       want_msys = false;
     }
   }
+  // single systems: the multi-line executor, except for solve pairs whose L
+  // rows carry many dependencies (>= 8 per row on average, e.g. the 27-point
+  // grid), where one warp per chain is faster (C5 single system: chain 2.71
+  // ms, multi-line 4.89 ms; C1's 5-point rows (3 per row) favour multi-line)
+  const bool dense_rows = (combo == 1 || combo == 8) && n > 0 && P->nnzL >= (int64_t)9 * n;
   const bool want_mline =
-      !P->use_msys && ((ex ? std::string(ex) == "mline" : P->nsys == 1) || combo == 2);
+      !P->use_msys &&
+      ((ex ? std::string(ex) == "mline" : (P->nsys == 1 && !dense_rows)) || combo == 2);
   if (P->use_msys) {
     // layouts built above
   } else if (want_mline && (combo == 1 || combo == 2 || combo == 4 || combo == 8)) {

@@ -5,10 +5,12 @@ it by oracle/Makefile).  Every array stored here is produced by the reference
 itself -- its generators (fixtures.hpp), make_state + run_sequential_reference
 + collect_outputs (kernels.hpp), build_g1/build_g2/inter_dag/joint_dag/
 level_info/compute_reuse (dag.hpp) and build_wavefront_schedule
-(executor.hpp) -- except combo 8 (forward L then backward L^T), which the
-reference lacks: its outputs come from the reference's own primitives
-composed as SURVEY.md 8(c) prescribes (sptrsv on P L^T P^T), checked here
-against a dense backward substitution.
+(executor.hpp) -- and combo 8 (forward L then backward L^T), which the
+reference lacks as a pair: its outputs come from the reference's own
+primitives composed as SURVEY.md 8(c) prescribes -- sptrsv (kernels.hpp:
+335-342) on L, then sptrsv on permute_symmetric(transpose(L), rev)
+(matrix.hpp:130-173), oracle/ref_driver.cpp ref_fwd_bwd -- and are checked
+here against the C oracle (bit for bit) and a dense backward substitution.
 
     python tests/golden/make_golden.py
 """
@@ -96,10 +98,11 @@ def main():
             out[f"{key}/wf_tags"] = tags
             out[f"{key}/wf_iters"] = iters
             out[f"{key}/wf_ptr"] = lp
-        # combo 8 (Deviation 1): forward solve by the reference (combo 1's
-        # first kernel), backward by the reference's own sptrsv on P L^T P^T,
-        # i.e. the oracle's restatement, pinned to a dense substitution.
-        got8 = orc.run_sequential(8, M, 7)
+        # combo 8 (Deviation 1): the reference's primitives composed
+        # (ref_fwd_bwd); the oracle must agree bit for bit, and the backward
+        # half must match a dense substitution
+        got8 = ref.fwd_bwd(M, ref.gen_vector(M.n, 7))
+        assert np.array_equal(got8, orc.run_sequential(8, M, 7))
         z = ref.state(1, M, 7).execute(0)[: M.n]
         D = np.tril(to_dense(M))
         x_dense = dense_backward(D, z)

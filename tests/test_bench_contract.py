@@ -48,10 +48,45 @@ def test_reference_arm_json_line(cfg):
 
 
 def test_reference_arm_other_ranks_exit_silently():
-    r = _run(["--impl", "reference", "--size", "12", "--steps", "2", "--warmup", "3"],
+    r = _run(["--impl", "reference", "--gpus", "2", "--size", "12", "--steps", "2", "--warmup", "3"],
              env={"RANK": "1", "WORLD_SIZE": "2", "LOCAL_RANK": "1"})
     assert r.returncode == 0, r.stderr
     assert r.stdout.strip() == ""
+
+
+def test_gpus_must_match_world_size():
+    r = _run(["--impl", "reference", "--gpus", "4", "--size", "12", "--steps", "2", "--warmup", "3"],
+             env={"RANK": "0", "WORLD_SIZE": "2", "LOCAL_RANK": "0"})
+    assert r.returncode != 0 and "WORLD_SIZE" in r.stderr
+
+
+@pytest.mark.skipif(not _reference_built(), reason="oracle/_ref not built")
+def test_gpus_flag_spawns_its_ranks():
+    """--gpus 2 without torchrun: bench.py launches its two ranks itself
+    (torch.distributed.run on 127.0.0.1); exactly one JSON line comes back."""
+    env = {k: "" for k in ()}
+    e = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference",
+                        "--gpus", "2", "--size", "10", "--steps", "2", "--warmup", "3"],
+                       cwd=ROOT, capture_output=True, text=True, timeout=600, env=e)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [l for l in r.stdout.splitlines() if l.strip().startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["impl"] == "reference"
+    assert d["config"]["global_systems"] == 8  # BASELINE's batch, whatever N
+
+
+@pytest.mark.skipif(not _reference_built(), reason="oracle/_ref not built")
+def test_reference_arm_matches_our_config_and_skips_the_package():
+    r = _run(["--impl", "reference", "--config", "5", "--size", "10", "--steps", "2",
+              "--warmup", "3"])
+    assert r.returncode == 0, r.stderr
+    d = json.loads(r.stdout.strip().splitlines()[-1])
+    assert d["package_loaded"] is False
+    import bench
+    assert d["config"]["workload"] == bench.CONFIG_NAME[5]
+    assert d["config"]["combo"] == 8 and d["config"]["global_systems"] == bench.GLOBAL_BATCH
 
 
 def test_warmup_floor():

@@ -161,3 +161,54 @@ def test_reference_partitioning_validator_is_discriminating(golden):
     nbad, msg = rs.validate_partitioning(np.array([0, 1]), np.array([0, len(tags)]),
                                          tags[::-1], iters[::-1])
     assert nbad > 0 and "unsatisfied" in msg
+
+
+needs_ref = pytest.mark.skipif(not Reference.available(), reason="oracle/_ref not built")
+
+
+@needs_ref
+@pytest.mark.parametrize("case", ("cfg5_16", "banded", "grid", "irregular"))
+def test_combo8_vs_reference_primitives(orc, case):
+    """Combo 8 (fwd L, bwd L^T) restated by the oracle equals the reference's
+    primitives composed as SURVEY.md 8(c) prescribes -- sptrsv on L, then on
+    permute_symmetric(transpose(L), rev) -- bit for bit, beyond the golden
+    matrices: C5's 27-point stencil (8 systems), banded, grid and an irregular
+    random pattern."""
+    ref = Reference()
+    if case == "cfg5_16":
+        M, vals = ref.config_matrix(5, 16, nsys_perturb=8)
+        systems = [Csc(M.n, M.colptr, M.rowidx, vals[s * M.nnz:(s + 1) * M.nnz]) for s in range(8)]
+    elif case == "banded":
+        systems = [ref.gen_banded_spd(3000, 40, 5)]
+    elif case == "grid":
+        systems = [ref.gen_grid_laplacian(40)]
+    else:
+        rng = np.random.default_rng(3)
+        n = 1500
+        D = np.zeros((n, n))
+        for i in range(n):
+            js = rng.integers(0, i + 1, size=rng.integers(0, 12))
+            D[i, js] = rng.uniform(-1, 0, size=len(js))
+            D[i, i] = 4.0 + rng.uniform(0, 1)
+        systems = [csc_from_dense(np.tril(D) + np.tril(D, -1).T)]
+    for s, Ms in enumerate(systems):
+        b = ref.gen_vector(Ms.n, 7 + s)
+        assert np.array_equal(orc.run_sequential(8, Ms, 7, vin=b), ref.fwd_bwd(Ms, b))
+
+
+@needs_ref
+@pytest.mark.parametrize("cfg", (1, 2, 3, 4, 5))
+def test_reference_arm_inputs_equal_the_packages(cfg):
+    """bench.py's reference arm generates its inputs from oracle/_ref (the
+    repo's fixtures.cpp compiled in under renamed symbols), never from
+    libsfgpu.so; they must be the very inputs our arm uses."""
+    import paper_2111_12238_b200 as sf
+    ref = Reference()
+    size = {1: 40, 2: 10, 3: 9, 4: 5000, 5: 12}[cfg]
+    A, B = ref.config_matrix(cfg, size), sf.config_matrix(cfg, size=size)
+    assert np.array_equal(A.colptr, B.colptr) and np.array_equal(A.rowidx, B.rowidx)
+    assert np.array_equal(A.values, B.values)
+    if cfg == 5:
+        _, v1 = ref.config_matrix(5, size, nsys_perturb=8, seed0=1004)
+        _, v2 = sf.config5_systems(size=size, nsys=8, seed0=1004)
+        assert np.array_equal(v1, v2)
