@@ -64,29 +64,59 @@ __device__ void trsv_row(int r, int s, int S, const int32_t* ptr, const int32_t*
 // ic0_column (kernels.hpp:214-242): the dense marker becomes a merge of
 // column k's sorted rows with column j's rows from L(k,j) on.  The column's
 // initial values come from lc_val (combo 5) or from fac (combo 7, written by
-// the DSCAL iteration of the same column).
+// the DSCAL iteration of the same column).  Short columns (<= WB entries)
+// keep their rows and sums in thread-local arrays and load each column j's
+// tail in one batch of independent loads before merging it, so a column costs
+// a few L2 round trips per predecessor rather than one per entry.
+constexpr int WB = 32;
+
 __device__ void ic0_col(int k, const ExecArgs& A, bool from_fac, int kernel) {
   const int c0 = __ldg(A.lc_ptr + k), c1 = __ldg(A.lc_ptr + k + 1);
   const int m = c1 - c0;
-  double* acc = A.work + c0;
-  for (int a = 0; a < m; ++a)
+  const bool local = m <= WB;
+  int rows[WB];
+  double accl[WB];
+  double* acc = local ? accl : A.work + c0;
+  for (int a = 0; a < m; ++a) {
+    if (local)
+      rows[a] = __ldg(A.lc_idx + c0 + a);
     acc[a] = from_fac ? ld_cg(A.fac + c0 + a) : __ldg(A.lc_val + c0 + a);
+  }
+#define ROW(a) (local ? rows[(a)] : __ldg(A.lc_idx + c0 + (a)))
   for (int q = __ldg(A.rv_ptr + k); q < __ldg(A.rv_ptr + k + 1); ++q) {
     const int j = __ldg(A.rv_col + q);
     const int pj = __ldg(A.rv_pos + q);
     const int pe = __ldg(A.lc_ptr + j + 1);
     const double lkj = ld_cg(A.fac + pj);
     int a = 0;
+    if (local && pe - pj <= WB) {
+      int tr[WB];
+      double tv[WB];
+      for (int u = 0; u < pe - pj; ++u) {
+        tr[u] = __ldg(A.lc_idx + pj + u);
+        tv[u] = ld_cg(A.fac + pj + u);
+      }
+      for (int u = 0; u < pe - pj; ++u) {
+        while (a < m && rows[a] < tr[u])
+          ++a;
+        if (a == m)
+          break;
+        if (rows[a] == tr[u])
+          acc[a] = fsub_mul(acc[a], lkj, tv[u]);
+      }
+      continue;
+    }
     for (int p = pj; p < pe; ++p) {
       const int i = __ldg(A.lc_idx + p);
-      while (a < m && __ldg(A.lc_idx + c0 + a) < i)
+      while (a < m && ROW(a) < i)
         ++a;
       if (a == m)
         break;
-      if (__ldg(A.lc_idx + c0 + a) == i)
+      if (ROW(a) == i)
         acc[a] = fsub_mul(acc[a], lkj, ld_cg(A.fac + p));
     }
   }
+#undef ROW
   const double d = acc[0];
   if (d <= 0.0)
     report_error(A.err, kernel, k, k);
@@ -98,14 +128,23 @@ __device__ void ic0_col(int k, const ExecArgs& A, bool from_fac, int kernel) {
 
 // ilu0_row (kernels.hpp:246-272) by merging row i with the pivot rows' upper
 // parts; initial values from ar_val (combo 6) or fac (combo 3, DSCAL'd).
+// Short rows keep columns and sums in thread-local arrays and load each
+// pivot row's upper part in one batch before merging it.
 __device__ void ilu0_row(int i, const ExecArgs& A, bool from_fac, int kernel) {
   const int r0 = __ldg(A.ar_ptr + i), r1 = __ldg(A.ar_ptr + i + 1);
   const int m = r1 - r0;
-  double* acc = A.work + r0;
-  for (int a = 0; a < m; ++a)
-    acc[a] = from_fac ? ld_cg(A.fac + r0 + a) : __ldg(A.ar_val + r0 + a);
+  const bool local = m <= WB;
+  int cols[WB];
+  double accl[WB];
+  double* acc = local ? accl : A.work + r0;
   for (int a = 0; a < m; ++a) {
-    const int k = __ldg(A.ar_idx + r0 + a);
+    if (local)
+      cols[a] = __ldg(A.ar_idx + r0 + a);
+    acc[a] = from_fac ? ld_cg(A.fac + r0 + a) : __ldg(A.ar_val + r0 + a);
+  }
+#define COL(a) (local ? cols[(a)] : __ldg(A.ar_idx + r0 + (a)))
+  for (int a = 0; a < m; ++a) {
+    const int k = COL(a);
     if (k >= i)
       break;
     const int dk = __ldg(A.diag + k);
@@ -116,17 +155,36 @@ __device__ void ilu0_row(int i, const ExecArgs& A, bool from_fac, int kernel) {
     acc[a] = lik;
     if (dk < 0)
       continue;
+    const int qe = __ldg(A.ar_ptr + k + 1);
     int b = a + 1;
-    for (int q = dk + 1; q < __ldg(A.ar_ptr + k + 1); ++q) {
+    if (local && qe - dk - 1 <= WB) {
+      int tc[WB];
+      double tv[WB];
+      for (int u = 0; u < qe - dk - 1; ++u) {
+        tc[u] = __ldg(A.ar_idx + dk + 1 + u);
+        tv[u] = ld_cg(A.fac + dk + 1 + u);
+      }
+      for (int u = 0; u < qe - dk - 1; ++u) {
+        while (b < m && cols[b] < tc[u])
+          ++b;
+        if (b == m)
+          break;
+        if (cols[b] == tc[u])
+          acc[b] = fsub_mul(acc[b], lik, tv[u]);
+      }
+      continue;
+    }
+    for (int q = dk + 1; q < qe; ++q) {
       const int j = __ldg(A.ar_idx + q);
-      while (b < m && __ldg(A.ar_idx + r0 + b) < j)
+      while (b < m && COL(b) < j)
         ++b;
       if (b == m)
         break;
-      if (__ldg(A.ar_idx + r0 + b) == j)
+      if (COL(b) == j)
         acc[b] = fsub_mul(acc[b], lik, ld_cg(A.fac + q));
     }
   }
+#undef COL
   for (int a = 0; a < m; ++a)
     A.fac[r0 + a] = acc[a];
 }
