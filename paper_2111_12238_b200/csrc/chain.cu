@@ -459,8 +459,11 @@ __global__ void __launch_bounds__(kThreads) k_chain(const ChainArgs A) {
             // wait phase: every row of the tile gathers its non-carry terms
             double acc = 0.0;
             if (cur.act) {
-              const double rv = cur.rhs != SENT ? __longlong_as_double((long long)cur.rhs)
-                                                : poll_f64(rhs_vec + (size_t)r * S + s, 0);
+              // only a published right-hand side (vmid) is polled: b is read
+              // once, and may hold any bit pattern
+              const double rv = (!rpoll || cur.rhs != SENT)
+                                    ? __longlong_as_double((long long)cur.rhs)
+                                    : poll_f64(rhs_vec + (size_t)r * S + s, 0);
               acc = wait_and_sum<S, CHN>(cur, rv, idx, val + s, xo + s);
               if (cur.d == 0.0)
                 report_error(A.err, kern, bwd ? A.n - 1 - r : r, r);
@@ -735,8 +738,10 @@ __global__ void __launch_bounds__(kSmThreads, COMBO == 1 ? 1 : SFG_CHAIN_MINB) k
         if (pass1) {
           double acc = 0.0;
           if (cact) {
-            acc = crhs != SENT ? __longlong_as_double((long long)crhs)
-                               : poll_f64(rhs_vec + (size_t)r * S + s, 0);
+            // only a published right-hand side (vmid) is polled: b is read
+            // once, and may hold any bit pattern
+            acc = (!rpoll || crhs != SENT) ? __longlong_as_double((long long)crhs)
+                                           : poll_f64(rhs_vec + (size_t)r * S + s, 0);
             const int m = ceend - cb < CHN ? ceend - cb : CHN;
             unsigned long long xx[CHN];
 #pragma unroll

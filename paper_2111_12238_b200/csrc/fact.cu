@@ -156,12 +156,41 @@ __global__ void k_list_stats(const int32_t* __restrict__ tptr, int32_t n,
   atomicMax(out + 1, mu);
 }
 
+__global__ void k_sum64(const int32_t* __restrict__ v, int64_t n, unsigned long long* out) {
+  unsigned long long acc = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    acc += (unsigned)v[i];
+  for (int o = 16; o > 0; o >>= 1)
+    acc += __shfl_down_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0)
+    atomicAdd(out, acc);
+}
+
+// Update lists are indexed with int32: a pattern whose total exceeds 2^31 - 1
+// updates (they grow faster than nnz) gets no lists -- out.count = -1, and
+// the *_warp_fits checks send the plan to the level-set executor.
 template <typename CountK, typename FillK>
 void build_lists(int32_t n, int64_t nnz, const int32_t* tptr, UpdateLists& out, cudaStream_t s,
                  CountK count, FillK fill) {
   DBuf<int32_t> cnt(nnz + 1);
   SFG_CUDA(cudaMemsetAsync(cnt.p, 0, sizeof(int32_t) * (size_t)(nnz + 1), s));
   count(cnt.p);
+  {
+    DBuf<unsigned long long> tot(1);
+    SFG_CUDA(cudaMemsetAsync(tot.p, 0, sizeof(unsigned long long), s));
+    k_sum64<<<grid_n(nnz), kFBlock, 0, s>>>(cnt.p, nnz, tot.p);
+    count_launch();
+    unsigned long long h = 0;
+    SFG_CUDA(cudaMemcpyAsync(&h, tot.p, sizeof(h), cudaMemcpyDeviceToHost, s));
+    SFG_CUDA(cudaStreamSynchronize(s));
+    if (h > (unsigned long long)INT32_MAX - 1) {
+      out.count = -1;
+      out.max_task = INT32_MAX;
+      out.max_updates = INT32_MAX;
+      return;
+    }
+  }
   out.ptr.alloc(nnz + 1);
   size_t bytes = 0;
   SFG_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, bytes, cnt.p, out.ptr.p, nnz + 1, s));
@@ -664,9 +693,11 @@ void build_ilu0_updates(const int32_t* ar_ptr, const int32_t* ar_idx, const int3
       });
 }
 
-bool ic0_warp_fits(const UpdateLists& up) { return up.max_task <= 32; }
+int fact_warps_per_block() { return kFBlock / 32; }
+
+bool ic0_warp_fits(const UpdateLists& up) { return up.count >= 0 && up.max_task <= 32; }
 bool ilu0_warp_fits(const UpdateLists& up) {
-  return up.max_task <= 32 && up.max_updates <= kMaxIluUpd;
+  return up.count >= 0 && up.max_task <= 32 && up.max_updates <= kMaxIluUpd;
 }
 
 void launch_ic0_warp(int combo, const ExecArgs& a, const UpdateLists& up, cudaStream_t s) {

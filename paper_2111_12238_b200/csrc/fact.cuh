@@ -44,6 +44,8 @@ void build_ilu0_updates(const int32_t* ar_ptr, const int32_t* ar_idx, const int3
 
 // Whether the warp executors cover every task of the plan (one lane per
 // column / row entry; ILU0 keeps each entry's updates in registers).
+// warps in one block of the factorization executors (occupancy sizing)
+int fact_warps_per_block();
 bool ic0_warp_fits(const UpdateLists& up);
 bool ilu0_warp_fits(const UpdateLists& up);
 

@@ -953,10 +953,6 @@ void build_mline_stream(const int32_t* ptr, const double* val, int32_t n, int di
 void launch_mline(const MLineArgs& a, cudaStream_t s) {
   if (a.seg_end <= a.seg_begin)
     return;
-  if (a.use_msys) {
-    launch_msys(a, s);
-    return;
-  }
   if (a.S == 1 && a.use_stream) {
     auto kern = a.stream_ch <= 2 ? k_mline1<2> : k_mline1<4>;
     const size_t smem = (size_t)(kMThreads / 32) *

@@ -55,14 +55,6 @@ struct MLineLayout {
   DBuf<int64_t> sofs;
   DBuf<int32_t> srow, scode;
   DBuf<double> sval;
-  // Multi-system executor (k_msys, B = 32 layout only; see msys.cu):
-  // per position p a record of mrec_w int32 {row, chained | early count << 8
-  // | late count << 16, ech early codes, lch late codes} and, per system
-  // pair, a value record of (ech + lch + 3) pairs {early values, late values,
-  // carry coefficient, diagonal, RN(1/diagonal)} (zero padding).
-  int32_t ech = 0, lch = 0, mrec_w = 0;
-  DBuf<int32_t> mrec;
-  DBuf<double> mval;
 };
 
 constexpr int32_t kStreamChn = 4;
@@ -81,15 +73,6 @@ void build_mline(const int32_t* ptr, const int32_t* idx, int32_t n, int dir, int
 // Widest dependency count (diagonal and carry excluded) over all rows.
 int32_t mline_width(const int32_t* ptr, const int32_t* idx, int32_t n, int dir,
                     const MLineLayout& L, cudaStream_t s);
-
-// Builds the k_msys records and value records for an S-system batch (S even).
-// Returns false (L.mrec/mval left empty) when no instantiated record shape
-// covers the rows' dependency split.
-bool build_msys(const int32_t* ptr, const double* val, int32_t n, int dir, int32_t S,
-                MLineLayout& L, cudaStream_t s);
-// Rewrites the value records from new values (same pattern).
-void refresh_msys_values(const int32_t* ptr, const double* val, int32_t n, int dir, int32_t S,
-                         MLineLayout& L, cudaStream_t s);
 
 struct MLineArgs {
   int combo = 0;
@@ -124,12 +107,6 @@ struct MLineArgs {
   const double *f_sval = nullptr, *b_sval = nullptr;
   bool use_stream = false;
   int32_t stream_ch = 4;
-  // multi-system lane-per-chain executor (k_msys): B = 32 layouts, records
-  // per position, a pair of systems per work item
-  bool use_msys = false;
-  int32_t ech = 0, lch = 0;
-  const int32_t *f_mrec = nullptr, *b_mrec = nullptr;
-  const double *f_mval = nullptr, *b_mval = nullptr;
   // diagnostics (SFG_TRACE): per work item {claim ns, first step ns, end ns,
   // stall cycles in cp.async waits << 32 | cycles in re-polls}
   unsigned long long* trace = nullptr;
@@ -139,6 +116,5 @@ struct MLineArgs {
 constexpr int32_t kMLineMaxChn = 12;
 
 void launch_mline(const MLineArgs& a, cudaStream_t s);
-void launch_msys(const MLineArgs& a, cudaStream_t s);
 
 } // namespace sfg

@@ -4,7 +4,6 @@
 // execute_unfused / collect_outputs (kernels.hpp, dag.hpp, executor.hpp).
 #include "../../include/sfgpu.h"
 #include "chain.cuh"
-#include "ell.cuh"
 #include "fact.cuh"
 #include "mline.cuh"
 #include "common.cuh"
@@ -76,17 +75,12 @@ struct sfg_plan {
   // as SFG_EXECUTOR=levels for ablations
   bool use_chain = false;
   ChainLayout ch_f, ch_b;
-  bool use_ell = false; // TMA-staged chain-ELL executor (batched combo 8)
-  bool use_ws = false;  // warp-specialised chain-ELL executor (batched combo 8)
-  EllLayout ell_f, ell_b;
-  int32_t ell_chn = 0;
   DBuf<int32_t> tail_ptr, tail_rows;
   std::vector<int32_t> row_maxcol; // (unused by the chain path; kept for stats)
   int32_t tile_rows = 0;           // chain tile height override (0 = chain_G default)
   DBuf<unsigned long long> trace;  // SFG_TRACE diagnostics
   // multi-chain warp executor (combos 1, 8; default)
   bool use_mline = false;
-  bool use_msys = false; // k_msys over the B = 32 layouts (batched solves)
   MLineLayout ml_f, ml_b;
   // warp-per-task factorization executors (combos 5, 6, 7)
   bool use_warpfac = false;
@@ -608,14 +602,24 @@ ExecArgs exec_args(sfg_plan* P) {
     // on a DAG of narrow levels the extra warps only spin beside the ones
     // on the critical path (C4, ~110 columns per level: 4 -> 2 blocks/SM,
     // 9.19 -> 8.70 ms); wide-level DAGs (C2, C3) keep full occupancy
+    // The same rule sizes the unfused comparator's launches.  Level width is
+    // the median over the waves (a few very wide levels beside a long narrow
+    // tail do not buy full occupancy; the 90th percentile gave C4 3 blocks/SM,
+    // 8.72 -> 8.89 ms).
     int look = 20;
     if (const char* e = getenv("SFG_FACT_LOOKAHEAD"))
-      look = atoi(e);
+      look = std::max(0, std::min(atoi(e), 100000));
     const int64_t waves = std::max<int64_t>(1, (int64_t)P->wave_ptr.size() - 1);
-    const double per_level = (double)P->n / (double)waves;
-    const double warps = look * per_level;
+    std::vector<int64_t> width((size_t)waves, 0);
+    for (int64_t w = 0; w + 1 < (int64_t)P->wave_ptr.size(); ++w)
+      width[(size_t)w] = P->wave_ptr[(size_t)w + 1] - P->wave_ptr[(size_t)w];
+    const size_t k50 = (size_t)(0.5 * (double)(waves - 1));
+    std::nth_element(width.begin(), width.begin() + k50, width.end());
+    const double per_level = (double)std::max<int64_t>(1, width[k50]);
+    const double warps = (double)look * per_level;
     if (look > 0)
-      a.blocks_per_sm = std::max(1, (int)std::ceil(warps / (8.0 * sm_count())));
+      a.blocks_per_sm = std::max(
+          1, (int)std::min(64.0, std::ceil(warps / ((double)fact_warps_per_block() * sm_count()))));
   }
   if (const char* e = getenv("SFG_BLOCKS_PER_SM"))
     a.blocks_per_sm = atoi(e);
@@ -708,40 +712,14 @@ void do_inspect(sfg_plan* P) {
   // executor choice: the multi-chain warp executor for single-system solve
   // pairs (latency-bound: in-warp dependencies go through shared memory),
   // the chain executor for batched systems; SFG_EXECUTOR overrides
-  bool want_msys = ex && std::string(ex) == "msys" && P->nsys >= 2 && P->nsys % 2 == 0 &&
-                   (combo == 1 || combo == 8);
-  if (want_msys) { // one chain per lane, system pairs (msys.cu); falls back to chains
-    int32_t max_len = 1 << 20;
-    if (const char* e = getenv("SFG_CHAIN_MAX"))
-      max_len = atoi(e);
-    build_mline(P->lr_ptr.p, P->lr_idx.p, n, +1, 1, max_len, P->ml_f, s);
-    bool ok = build_msys(P->lr_ptr.p, P->lr_val.p, n, +1, P->nsys, P->ml_f, s);
-    if (ok && combo == 8) {
-      build_mline(P->lt_ptr.p, P->lt_idx.p, n, -1, 1, max_len, P->ml_b, s);
-      ok = build_msys(P->lt_ptr.p, P->lt_val.p, n, -1, P->nsys, P->ml_b, s);
-    }
-    if (ok && combo == 8 && (P->ml_f.ech != P->ml_b.ech || P->ml_f.lch != P->ml_b.lch))
-      ok = false; // one kernel instantiation serves both segments
-    if (ok) {
-      P->use_mline = true;
-      P->use_msys = true;
-    } else {
-      P->ml_f = MLineLayout{};
-      P->ml_b = MLineLayout{};
-      want_msys = false;
-    }
-  }
   // single systems: the multi-line executor, except for solve pairs whose L
   // rows carry many dependencies (>= 8 per row on average, e.g. the 27-point
   // grid), where one warp per chain is faster (C5 single system: chain 2.71
   // ms, multi-line 4.89 ms; C1's 5-point rows (3 per row) favour multi-line)
   const bool dense_rows = (combo == 1 || combo == 8) && n > 0 && P->nnzL >= (int64_t)9 * n;
   const bool want_mline =
-      !P->use_msys &&
-      ((ex ? std::string(ex) == "mline" : (P->nsys == 1 && !dense_rows)) || combo == 2);
-  if (P->use_msys) {
-    // layouts built above
-  } else if (want_mline && (combo == 1 || combo == 2 || combo == 4 || combo == 8)) {
+      (ex ? std::string(ex) == "mline" : (P->nsys == 1 && !dense_rows)) || combo == 2;
+  if (want_mline && (combo == 1 || combo == 2 || combo == 4 || combo == 8)) {
     int32_t max_len = 1 << 20;
     if (const char* e = getenv("SFG_CHAIN_MAX"))
       max_len = atoi(e);
@@ -750,7 +728,7 @@ void do_inspect(sfg_plan* P) {
       build_mline(P->lt_ptr.p, P->lt_idx.p, n, -1, P->nsys, max_len, P->ml_b, s);
     P->use_mline = true;
     const char* se = getenv("SFG_MLINE_STREAM");
-    if (P->nsys == 1 && !P->use_msys && !(se && std::string(se) == "0")) { // step streams (k_mline1)
+    if (P->nsys == 1 && !(se && std::string(se) == "0")) { // step streams (k_mline1)
       build_mline_stream(P->lr_ptr.p, P->lr_val.p, n, +1, P->ml_f, s);
       if (combo == 8)
         build_mline_stream(P->lt_ptr.p, P->lt_val.p, n, -1, P->ml_b, s);
@@ -762,17 +740,13 @@ void do_inspect(sfg_plan* P) {
     if (getenv("SFG_MLINE_STATS")) {
       for (const MLineLayout* L : {&P->ml_f, &P->ml_b})
         if (L->nchain > 0)
-          fprintf(stderr, "mline dir=%d nchain=%d ngroup=%d levels=%d max_steps=%d est_steps=%d width=%d%s\n",
-                  L->dir, L->nchain, L->ngroup, L->nlevels, L->max_steps, L->est_steps, L->CHN,
-                  P->use_msys ? (" msys ech=" + std::to_string(L->ech) + " lch=" +
-                                 std::to_string(L->lch)).c_str()
-                              : "");
+          fprintf(stderr, "mline dir=%d nchain=%d ngroup=%d levels=%d max_steps=%d est_steps=%d width=%d\n",
+                  L->dir, L->nchain, L->ngroup, L->nlevels, L->max_steps, L->est_steps, L->CHN);
     }
     if (getenv("SFG_TRACE")) {
       P->trace_tiles = 4;
-      const int64_t items = ((int64_t)P->ml_f.ngroup + (n + 31) / 32 +
-                             (combo == 8 ? P->ml_b.ngroup : P->ml_f.ngroup)) *
-                            (P->use_msys ? P->nsys / 2 : 1);
+      const int64_t items = (int64_t)P->ml_f.ngroup + (n + 31) / 32 +
+                            (combo == 8 ? P->ml_b.ngroup : P->ml_f.ngroup);
       P->trace.alloc(items * 4);
       SFG_CUDA(cudaMemsetAsync(P->trace.p, 0, sizeof(unsigned long long) * items * 4, s));
     }
@@ -803,20 +777,6 @@ void do_inspect(sfg_plan* P) {
       build_chains(P->lt_ptr.p, P->lt_idx.p, n, -1, G, CS, max_len, P->ch_b, s);
     if (combo == 4)
       build_tails(P->ch_f, P->ar_ptr.p, P->ar_idx.p, n, P->tail_ptr, P->tail_rows, s);
-    const char* ell_env = getenv("SFG_ELL");
-    const bool want_ws = ex && std::string(ex) == "ws" && combo == 8 && P->nsys >= 4;
-    if (combo == 8 && P->nsys >= 2 && ((ell_env && std::string(ell_env) == "1") || want_ws)) {
-      const int32_t w = std::max(ell_width(P->lr_ptr.p, P->lr_idx.p, n, +1, P->ch_f, s),
-                                 ell_width(P->lt_ptr.p, P->lt_idx.p, n, -1, P->ch_b, s));
-      const int32_t chn = std::max(4, (w + 3) / 4 * 4);
-      if (chn <= kEllMaxWidth) {
-        P->ell_chn = chn;
-        build_ell(P->lr_ptr.p, P->lr_idx.p, P->lr_val.p, n, P->nsys, +1, chn, P->ch_f, P->ell_f, s);
-        build_ell(P->lt_ptr.p, P->lt_idx.p, P->lt_val.p, n, P->nsys, -1, chn, P->ch_b, P->ell_b, s);
-        P->use_ell = !want_ws;
-        P->use_ws = want_ws;
-      }
-    }
     if (getenv("SFG_TRACE")) {
       P->trace_tiles = getenv("SFG_TRACE_TILES") ? atoi(getenv("SFG_TRACE_TILES")) : 160;
       const int64_t items = (int64_t)P->ch_f.nbatch + P->ch_b.nbatch;
@@ -827,43 +787,6 @@ void do_inspect(sfg_plan* P) {
   }
   SFG_CUDA(cudaStreamSynchronize(s));
   P->inspected = true;
-}
-
-EllArgs ell_args(sfg_plan* P) {
-  EllArgs a;
-  a.n = P->n;
-  a.S = P->nsys;
-  if (const char* e = getenv("SFG_WS_SLOTS"))
-    a.ws_slots = atoi(e);
-  if (const char* e = getenv("SFG_WS_PAIRS"))
-    a.ws_pairs = atoi(e);
-  if (const char* e = getenv("SFG_WS_FENCE"))
-    a.ws_fence = atoi(e);
-  a.counter = P->counter.p;
-  a.err = P->err.p;
-  a.f_cstart = P->ch_f.cstart.p;
-  a.f_corder = P->ch_f.corder.p;
-  a.f_bptr = P->ch_f.batch_ptr.p;
-  a.f_level = P->ch_f.clevel.p;
-  a.f_nbatch = P->ch_f.nbatch;
-  a.f_eidx = P->ell_f.eidx.p;
-  a.f_eval = P->ell_f.eval.p;
-  a.b_cstart = P->ch_b.cstart.p;
-  a.b_corder = P->ch_b.corder.p;
-  a.b_bptr = P->ch_b.batch_ptr.p;
-  a.b_level = P->ch_b.clevel.p;
-  a.b_eidx = P->ell_b.eidx.p;
-  a.b_eval = P->ell_b.eval.p;
-  if (P->trace.p) {
-    a.trace = P->trace.p;
-    a.trace_tiles = P->trace_tiles;
-  }
-  a.vin = P->vin.p;
-  a.vmid = P->vmid.p;
-  a.vout = P->vout.p;
-  if (const char* e = getenv("SFG_BLOCKS_PER_SM"))
-    a.blocks_per_sm = atoi(e);
-  return a;
 }
 
 MLineArgs mline_args(sfg_plan* P) {
@@ -908,13 +831,6 @@ MLineArgs mline_args(sfg_plan* P) {
   a.trace = P->trace.p;
   a.use_stream = P->ml_f.stream && L2.stream && P->ml_f.sch == L2.sch;
   a.stream_ch = P->ml_f.sch;
-  a.use_msys = P->use_msys;
-  a.ech = P->ml_f.ech;
-  a.lch = P->ml_f.lch;
-  a.f_mrec = P->ml_f.mrec.p;
-  a.b_mrec = L2.mrec.p;
-  a.f_mval = P->ml_f.mval.p;
-  a.b_mval = L2.mval.p;
   a.f_sofs = P->ml_f.sofs.p;
   a.f_srow = P->ml_f.srow.p;
   a.f_scode = P->ml_f.scode.p;
@@ -927,11 +843,6 @@ MLineArgs mline_args(sfg_plan* P) {
     a.sleep_ns = (unsigned)atoi(e);
   if (const char* e = getenv("SFG_MLINE_DX"))
     a.lookahead = atoi(e);
-  if (P->use_msys) { // k_msys: L2 prefetch distance beyond the record distance
-    a.lookahead = 0;
-    if (const char* e = getenv("SFG_MSYS_PF"))
-      a.lookahead = atoi(e);
-  }
   if (const char* e = getenv("SFG_BLOCKS_PER_SM"))
     a.blocks_per_sm = atoi(e);
   return a;
@@ -1265,17 +1176,7 @@ void exec_fused_impl(sfg_plan* P, cudaEvent_t kb, cudaEvent_t ke) {
   }
   launch_prep(r, nr, P->counter.p, P->err.p, P->stream);
   SFG_CUDA(cudaEventRecord(kb, P->stream));
-  if (P->use_ws) {
-    EllArgs e = ell_args(P);
-    e.seg_begin = 0;
-    e.seg_end = P->ch_f.nbatch + P->ch_b.nbatch;
-    launch_chain_ws(e, P->ell_chn, P->stream);
-  } else if (P->use_ell) {
-    EllArgs e = ell_args(P);
-    e.seg_begin = 0;
-    e.seg_end = P->ch_f.nbatch + P->ch_b.nbatch;
-    launch_chain_ell(e, P->ell_chn, P->stream);
-  } else if (P->use_mline) {
+  if (P->use_mline) {
     MLineArgs m = mline_args(P);
     m.seg_begin = 0;
     m.seg_end = m.f_ngroup + m.b_ngroup;
@@ -1359,29 +1260,6 @@ void exec_unfused_impl(sfg_plan* P, cudaEvent_t kb, cudaEvent_t ke, int which = 
   if (k1)
     launch_prep(r1, n1, P->counter.p, P->err.p, P->stream);
   SFG_CUDA(cudaEventRecord(kb, P->stream));
-  if (P->use_ell || P->use_ws) {
-    EllArgs e = ell_args(P);
-    auto launch = [&](const EllArgs& x) {
-      if (P->use_ws)
-        launch_chain_ws(x, P->ell_chn, P->stream);
-      else
-        launch_chain_ell(x, P->ell_chn, P->stream);
-    };
-    if (k1) {
-      e.seg_begin = 0;
-      e.seg_end = P->ch_f.nbatch;
-      launch(e);
-    }
-    if (k2) {
-      FillRegion r2[1] = {{P->vout.p, nv}};
-      launch_prep(r2, 1, P->counter.p, nullptr, P->stream);
-      e.seg_begin = P->ch_f.nbatch;
-      e.seg_end = P->ch_f.nbatch + P->ch_b.nbatch;
-      launch(e);
-    }
-    SFG_CUDA(cudaEventRecord(ke, P->stream));
-    return;
-  }
   if (P->use_mline) {
     MLineArgs m = mline_args(P);
     if (k1) {
@@ -1585,12 +1463,11 @@ sfg_status sfg_plan_destroy(sfg_plan* P) {
       }
     } else if (P->trace.p && P->use_mline) {
       // SFG_TRACE=<path>: {items, 4, fwd items, data[items*4]} (see MLineArgs::trace)
-      const int64_t items = ((int64_t)P->ml_f.ngroup + (P->combo == 8 ? P->ml_b.ngroup : P->ml_f.ngroup)) *
-                            (P->use_msys ? P->nsys / 2 : 1);
+      const int64_t items = (int64_t)P->ml_f.ngroup + (P->combo == 8 ? P->ml_b.ngroup : P->ml_f.ngroup);
       std::vector<unsigned long long> h((size_t)(items * 4));
       cudaMemcpy(h.data(), P->trace.p, sizeof(unsigned long long) * h.size(), cudaMemcpyDeviceToHost);
       if (FILE* f = fopen(getenv("SFG_TRACE"), "wb")) {
-        const int64_t hdr[3] = {items, 4, P->ml_f.ngroup * (P->use_msys ? P->nsys / 2 : 1)};
+        const int64_t hdr[3] = {items, 4, P->ml_f.ngroup};
         fwrite(hdr, sizeof(hdr), 1, f);
         fwrite(h.data(), sizeof(unsigned long long), h.size(), f);
         fclose(f);
@@ -1766,15 +1643,6 @@ sfg_status sfg_set_values(sfg_plan* P, const double* values_host) {
       build_mline_stream(P->lr_ptr.p, P->lr_val.p, n, +1, P->ml_f, s);
       if (c == 8)
         build_mline_stream(P->lt_ptr.p, P->lt_val.p, n, -1, P->ml_b, s);
-    }
-    if (P->use_msys) { // so do the k_msys value records
-      refresh_msys_values(P->lr_ptr.p, P->lr_val.p, n, +1, S, P->ml_f, s);
-      if (c == 8)
-        refresh_msys_values(P->lt_ptr.p, P->lt_val.p, n, -1, S, P->ml_b, s);
-    }
-    if (P->use_ell || P->use_ws) { // the chain-ELL records hold copies of the values
-      build_ell(P->lr_ptr.p, P->lr_idx.p, P->lr_val.p, n, S, +1, P->ell_chn, P->ch_f, P->ell_f, s);
-      build_ell(P->lt_ptr.p, P->lt_idx.p, P->lt_val.p, n, S, -1, P->ell_chn, P->ch_b, P->ell_b, s);
     }
     SFG_CUDA(cudaGetLastError());
     return SFG_OK;
@@ -2226,7 +2094,7 @@ void build_partition(sfg_plan* P, Partition& V) {
     }
     return;
   }
-  if (P->use_chain || P->use_ell) {
+  if (P->use_chain) {
     chain_levels(V, P->ch_f, 1, c == 1);
     if (c == 8)
       chain_levels(V, P->ch_b, 2, false);

@@ -135,3 +135,43 @@ def test_batched_random_patterns(orc, n, per_row, span, nsys):
                 want = orc.run_sequential(combo, Ms, 7, vin=vin[s * n:(s + 1) * n])
                 assert np.array_equal(got[s], want), (combo, nsys, s)
         st.close()
+
+
+_ALLONES_SCRIPT = r"""
+import sys, numpy as np
+sys.path.insert(0, sys.argv[1])
+import paper_2111_12238_b200 as sf
+from oracle.oracle import Csc, Oracle
+nsys = int(sys.argv[2])
+M, vals = sf.config5_systems(size=10, nsys=nsys)
+n, nnz = M.n, M.nnz
+vin = np.concatenate([sf.gen_vector(n, 7 + s) for s in range(nsys)])
+vin.view(np.uint64)[3] = np.uint64(0xFFFFFFFFFFFFFFFF)  # b holding the all-ones NaN word
+for combo in (8, 1):
+    st = sf.make_state(combo, M, nsys=nsys, values=vals, vin=vin)
+    st.execute_fused()
+    got = st.collect_outputs().reshape(nsys, 2 * n)
+    for s in range(nsys):
+        want = Oracle().run_sequential(combo, Csc(n, M.colptr, M.rowidx, vals[s*nnz:(s+1)*nnz]), 7,
+                                       vin=vin[s*n:(s+1)*n])
+        assert np.array_equal(np.isnan(got[s]), np.isnan(want)), (combo, s)
+        ok = ~np.isnan(want)
+        assert np.array_equal(got[s][ok], want[ok]), (combo, s)
+print("OK")
+"""
+
+
+@pytest.mark.parametrize("nsys", (1, 8))
+def test_rhs_with_the_sentinel_bit_pattern(nsys, tmp_path):
+    """A right-hand side holding the all-ones word (a NaN the executors use as
+    "not yet published") is input, not a flag: the solve must finish and
+    propagate the NaN like the reference.  Run in a child with a
+    timeout so a regression cannot hang the device."""
+    import subprocess
+    import sys as _s
+    from conftest import ROOT
+    script = tmp_path / "allones.py"
+    script.write_text(_ALLONES_SCRIPT)
+    r = subprocess.run([_s.executable, str(script), ROOT, str(nsys)], capture_output=True, text=True,
+                       timeout=120)
+    assert r.returncode == 0 and r.stdout.strip().endswith("OK"), r.stdout + r.stderr

@@ -390,10 +390,17 @@ def test_alternative_executors_golden(golden, monkeypatch, executor, name):
         _check_linear_extension(st, st.dag(3))
 
 
-@pytest.mark.parametrize("executor,nsys", (("mline", 1), ("mline", 2), ("mline", 8), ("mline", 32),
-                                            ("ws", 4), ("ws", 8), ("ws", 16), ("ws", 32)))
-def test_mline_executor_vs_oracle(orc, monkeypatch, executor, nsys):
+@pytest.mark.parametrize("executor,nsys,rows", (("mline", 1, 0), ("mline", 2, 0), ("mline", 8, 0),
+                                                 ("mline", 32, 0), ("chain", 1, 0), ("chain", 1, 1),
+                                                 ("chain", 1, 8), ("chain", 2, 2), ("chain", 2, 16),
+                                                 ("chain", 4, 8), ("chain", 8, 2), ("chain", 16, 0),
+                                                 ("chain", 32, 0)))
+def test_mline_executor_vs_oracle(orc, monkeypatch, executor, nsys, rows):
+    """The 27-point grid through the multi-line and chain executors at every
+    batch size, including non-default chain tile heights (SFG_CHAIN_G)."""
     monkeypatch.setenv("SFG_EXECUTOR", executor)
+    if rows:
+        monkeypatch.setenv("SFG_CHAIN_G", str(rows))
     M, vals = sf.config5_systems(size=24, nsys=nsys)
     n, nnz = M.n, M.nnz
     vin = np.concatenate([sf.gen_vector(n, 7 + s) for s in range(nsys)])
@@ -617,34 +624,6 @@ def test_spmv_rows_rejects_bad_ranges():
     with pytest.raises(Exception):
         st.spmv_rows(0, M.n + 1, 1, 1)
     st.close()
-
-
-@pytest.mark.parametrize("nsys", (2, 8))
-def test_msys_executor_vs_oracle(orc, monkeypatch, capfd, nsys):
-    """SFG_EXECUTOR=msys (one chain per lane, system pairs; msys.cu) on a
-    27-point grid whose planes are one 32-line group each."""
-    monkeypatch.setenv("SFG_EXECUTOR", "msys")
-    monkeypatch.setenv("SFG_MLINE_STATS", "1")
-    M, vals = sf.config5_systems(size=32, nsys=nsys)
-    n, nnz = M.n, M.nnz
-    vin = np.concatenate([sf.gen_vector(n, 7 + s) for s in range(nsys)])
-    for combo in (8, 1):
-        st = sf.make_state(combo, M, nsys=nsys, values=vals, vin=vin).inspect()
-        assert "msys ech=" in capfd.readouterr().err  # the executor really ran
-        st.execute_fused()
-        got = st.collect_outputs().reshape(nsys, 2 * n)
-        for s in range(nsys):
-            Ms = Csc(n, M.colptr, M.rowidx, vals[s * nnz:(s + 1) * nnz])
-            want = orc.run_sequential(combo, Ms, 7, vin=vin[s * n:(s + 1) * n])
-            assert np.array_equal(got[s], want)
-        # new values through set_values refresh the value records
-        v2 = vals * 1.01
-        st.set_values(v2)
-        st.execute_fused()
-        got = st.collect_outputs().reshape(nsys, 2 * n)
-        Ms = Csc(n, M.colptr, M.rowidx, v2[:nnz])
-        assert np.array_equal(got[0], orc.run_sequential(combo, Ms, 7, vin=vin[:n]))
-        st.close()
 
 
 # ---------------------------------------------------------------------------
