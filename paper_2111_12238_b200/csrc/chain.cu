@@ -355,7 +355,7 @@ __global__ void __launch_bounds__(kThreads) k_chain(const ChainArgs A) {
     const int c = __ldg(corder + __ldg(bptr + bi));
     const int p0 = __ldg(cstart + c);
     const int len = __ldg(cstart + c + 1) - p0;
-    const int skew = __ldg(clev + c) % G;
+    const int skew = (__ldg(clev + c) * A.skew_mul) % G;
     const int ntiles = (len + skew + G - 1) / G;
     double* xo = bwd ? A.vout : A.vmid;
     const double* rhs_vec = bwd ? A.vmid : A.vin;
@@ -604,7 +604,7 @@ __global__ void __launch_bounds__(kSmThreads, COMBO == 1 ? 1 : SFG_CHAIN_MINB) k
     const int c = __ldg(corder + __ldg(bptr + bi));
     const int p0 = __ldg(cstart + c);
     const int len = __ldg(cstart + c + 1) - p0;
-    const int skew = __ldg(clev + c) % G;
+    const int skew = (__ldg(clev + c) * A.skew_mul) % G;
     const int ntiles = (len + skew + G - 1) / G;
     double* xo = bwd ? A.vout : A.vmid;
     const double* rhs_vec = bwd ? A.vmid : A.vin;

@@ -77,6 +77,10 @@ struct ChainArgs {
   double* vout = nullptr;
   int blocks_per_sm = 0;
   int tile_rows = 0; // tile height override (0 = chain_G's default)
+  // tile skew per chain level, in rows: a chain at level l starts its tiles
+  // (l * skew_mul) mod G rows early (1: a consumer tile needs the whole
+  // same-index tile of its previous-level producers)
+  int skew_mul = 1;
   unsigned bwd_gate = 500; // ns a backward chain's first lane sleeps per check (0 = off)
   // optional timeline trace: per (work item, tile) {claim, partial done,
   // carry done} in %globaltimer ns (diagnostics only; null in production)

@@ -873,6 +873,8 @@ ChainArgs chain_args(sfg_plan* P) {
   a.b_nbatch = P->ch_b.nbatch;
   a.tail_ptr = P->tail_ptr.p;
   a.tile_rows = P->tile_rows;
+  if (const char* e = getenv("SFG_CHAIN_SKEW"))
+    a.skew_mul = atoi(e);
   a.tail_rows = P->tail_rows.p;
   if (const char* e = getenv("SFG_BWD_GATE"))
     a.bwd_gate = (unsigned)atoi(e);
