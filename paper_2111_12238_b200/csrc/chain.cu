@@ -632,6 +632,31 @@ __global__ void __launch_bounds__(kSmThreads, COMBO == 1 ? 1 : SFG_CHAIN_MINB) k
     double cd = 1.0, cvc = 0.0, crd = 1.0;
     unsigned long long crhs = 0;
     double carry = 0.0, carry2 = 0.0;
+    if (bwd && pass1 && (A.phase & 1) && A.bwd_reset) {
+      // Fused fwd -> bwd: the backward outputs are reset here, not by k_prep
+      // before the launch.  The first bwd_reset_items backward work items --
+      // claimed while the forward solve still runs its last levels -- each
+      // set one slice of vout to SENT, and every backward chain waits for
+      // all slices before it reads a vout word (the unfused pair must reset
+      // vout between its two launches).
+      if (bi < A.bwd_reset_items) {
+        const int64_t w2 = A.bwd_reset_words / 2; // 16-byte stores
+        const int64_t per = (w2 + A.bwd_reset_items - 1) / A.bwd_reset_items;
+        const int64_t lo = per * bi, hi = min(w2, lo + per);
+        ulonglong2* p2 = reinterpret_cast<ulonglong2*>(A.bwd_reset);
+        for (int64_t i = lo + lane; i < hi; i += 32)
+          p2[i] = make_ulonglong2(SENT, SENT);
+        __syncwarp();
+        if (lane == 0) {
+          __threadfence();
+          atomicAdd(A.reset_done, 1ull);
+        }
+      }
+      if (lane == 0)
+        while (ld_relaxed_u64(A.reset_done) < (unsigned long long)A.bwd_reset_items)
+          __nanosleep(200);
+      __threadfence();
+    }
     if (bwd && pass1 && (A.phase & 1) && A.bwd_gate) { // fused launch only
       // a backward chain cannot start before the forward solve has reached
       // its first right-hand side: one lane sleeps on that word instead of

@@ -81,6 +81,13 @@ struct ChainArgs {
   // (l * skew_mul) mod G rows early (1: a consumer tile needs the whole
   // same-index tile of its previous-level producers)
   int skew_mul = 1;
+  // fused combo 8 (k_chain_sm): the backward outputs (vout, bwd_reset_words
+  // 8-byte words) are reset in-kernel by the first bwd_reset_items backward
+  // items; reset_done counts the finished slices (null: k_prep resets vout)
+  double* bwd_reset = nullptr;
+  int64_t bwd_reset_words = 0;
+  int32_t bwd_reset_items = 0;
+  unsigned long long* reset_done = nullptr;
   unsigned bwd_gate = 500; // ns a backward chain's first lane sleeps per check (0 = off)
   // optional timeline trace: per (work item, tile) {claim, partial done,
   // carry done} in %globaltimer ns (diagnostics only; null in production)

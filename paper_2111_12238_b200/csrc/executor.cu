@@ -382,7 +382,8 @@ __global__ void k_prep(const PrepArgs P) {
   const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   if (tid == 0) {
-    *P.counter = 0ull;
+    P.counter[0] = 0ull;
+    P.counter[1] = 0ull; // auxiliary counter (chain.cu: backward reset slices)
     if (P.err)
       *P.err = ~0ull;
   }

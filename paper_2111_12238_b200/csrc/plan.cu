@@ -556,7 +556,7 @@ void build_plan(sfg_plan* P, const int32_t* colptr, const int32_t* rowidx,
       SFG_CUDA(cudaMemsetAsync(P->vmid.p + nv, 0, sizeof(double) * (size_t)S, s));
     }
   }
-  P->counter.alloc(1);
+  P->counter.alloc(2); // ticket counter + auxiliary counter
   P->err.alloc(1);
   SFG_CUDA(cudaStreamSynchronize(s));
 }
@@ -1156,12 +1156,17 @@ void exec_fused_impl(sfg_plan* P, cudaEvent_t kb, cudaEvent_t ke) {
   const int64_t nv = (int64_t)P->n * P->nsys;
   FillRegion r[3];
   int nr = 0;
+  // fused fwd -> bwd on the batched chain executor resets vout in-kernel
+  // (ChainArgs::bwd_reset): k_prep only resets vmid
+  const bool inkernel_reset = P->combo == 8 && P->use_chain && P->nsys >= 2 && P->ch_b.nbatch > 0 &&
+                              nv % 2 == 0 && !getenv("SFG_PREP_VOUT");
   switch (P->combo) {
   case 1:
   case 2:
   case 8:
     r[nr++] = {P->vmid.p, nv};
-    r[nr++] = {P->vout.p, nv};
+    if (!inkernel_reset)
+      r[nr++] = {P->vout.p, nv};
     break;
   case 4:
     r[nr++] = {P->vmid.p, nv};
@@ -1186,6 +1191,12 @@ void exec_fused_impl(sfg_plan* P, cudaEvent_t kb, cudaEvent_t ke) {
   } else if (P->use_chain) {
     ChainArgs b = chain_args(P);
     b.phase = 3;
+    if (inkernel_reset) {
+      b.bwd_reset = P->vout.p;
+      b.bwd_reset_words = nv;
+      b.bwd_reset_items = std::min<int32_t>(P->ch_b.nbatch, 512);
+      b.reset_done = P->counter.p + 1;
+    }
     b.seg_begin = 0;
     b.seg_end = P->ch_f.nbatch + (P->combo == 8 ? P->ch_b.nbatch : 0);
     launch_chain(b, P->stream);
