@@ -632,17 +632,19 @@ __global__ void __launch_bounds__(kSmThreads, COMBO == 1 ? 1 : SFG_CHAIN_MINB) k
     double cd = 1.0, cvc = 0.0, crd = 1.0;
     unsigned long long crhs = 0;
     double carry = 0.0, carry2 = 0.0;
-    if (bwd && pass1 && (A.phase & 1) && A.bwd_reset) {
+    if (COMBO == 8 && (A.phase & 1) && A.bwd_reset) {
       // Fused fwd -> bwd: the backward outputs are reset here, not by k_prep
-      // before the launch.  The first bwd_reset_items backward work items --
-      // claimed while the forward solve still runs its last levels -- each
-      // set one slice of vout to SENT, and every backward chain waits for
-      // all slices before it reads a vout word (the unfused pair must reset
-      // vout between its two launches).
-      if (bi < A.bwd_reset_items) {
+      // before the launch.  The last bwd_reset_items forward work items --
+      // the top levels, claimed long before their producers finish, so their
+      // warps would otherwise only wait -- each set one slice of vout to
+      // SENT first; every backward chain waits for all slices before it
+      // reads a vout word.  (The unfused pair resets vout between its two
+      // launches.)
+      const int ri = A.f_nbatch - 1 - item;
+      if (!bwd && ri < A.bwd_reset_items) {
         const int64_t w2 = A.bwd_reset_words / 2; // 16-byte stores
         const int64_t per = (w2 + A.bwd_reset_items - 1) / A.bwd_reset_items;
-        const int64_t lo = per * bi, hi = min(w2, lo + per);
+        const int64_t lo = per * ri, hi = min(w2, lo + per);
         ulonglong2* p2 = reinterpret_cast<ulonglong2*>(A.bwd_reset);
         for (int64_t i = lo + lane; i < hi; i += 32)
           p2[i] = make_ulonglong2(SENT, SENT);
@@ -652,10 +654,12 @@ __global__ void __launch_bounds__(kSmThreads, COMBO == 1 ? 1 : SFG_CHAIN_MINB) k
           atomicAdd(A.reset_done, 1ull);
         }
       }
-      if (lane == 0)
-        while (ld_relaxed_u64(A.reset_done) < (unsigned long long)A.bwd_reset_items)
-          __nanosleep(200);
-      __threadfence();
+      if (bwd) {
+        if (lane == 0)
+          while (ld_relaxed_u64(A.reset_done) < (unsigned long long)A.bwd_reset_items)
+            __nanosleep(200);
+        __threadfence();
+      }
     }
     if (bwd && pass1 && (A.phase & 1) && A.bwd_gate) { // fused launch only
       // a backward chain cannot start before the forward solve has reached

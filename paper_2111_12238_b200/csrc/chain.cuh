@@ -82,7 +82,7 @@ struct ChainArgs {
   // same-index tile of its previous-level producers)
   int skew_mul = 1;
   // fused combo 8 (k_chain_sm): the backward outputs (vout, bwd_reset_words
-  // 8-byte words) are reset in-kernel by the first bwd_reset_items backward
+  // 8-byte words) are reset in-kernel by the last bwd_reset_items forward
   // items; reset_done counts the finished slices (null: k_prep resets vout)
   double* bwd_reset = nullptr;
   int64_t bwd_reset_words = 0;

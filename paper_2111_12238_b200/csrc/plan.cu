@@ -1158,7 +1158,7 @@ void exec_fused_impl(sfg_plan* P, cudaEvent_t kb, cudaEvent_t ke) {
   int nr = 0;
   // fused fwd -> bwd on the batched chain executor resets vout in-kernel
   // (ChainArgs::bwd_reset): k_prep only resets vmid
-  const bool inkernel_reset = P->combo == 8 && P->use_chain && P->nsys >= 2 && P->ch_b.nbatch > 0 &&
+  const bool inkernel_reset = P->combo == 8 && P->use_chain && P->nsys >= 2 && P->ch_f.nbatch > 0 &&
                               nv % 2 == 0 && !getenv("SFG_PREP_VOUT");
   switch (P->combo) {
   case 1:
@@ -1194,7 +1194,7 @@ void exec_fused_impl(sfg_plan* P, cudaEvent_t kb, cudaEvent_t ke) {
     if (inkernel_reset) {
       b.bwd_reset = P->vout.p;
       b.bwd_reset_words = nv;
-      b.bwd_reset_items = std::min<int32_t>(P->ch_b.nbatch, 512);
+      b.bwd_reset_items = std::min<int32_t>(P->ch_f.nbatch, 512);
       b.reset_done = P->counter.p + 1;
     }
     b.seg_begin = 0;
