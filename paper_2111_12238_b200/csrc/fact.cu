@@ -638,6 +638,152 @@ __global__ void __launch_bounds__(kFBlock, MAXU <= 4 ? SFG_ILU_MINB4 : 1) k_ilu0
   }
 }
 
+// ILU0 rows packed PK = 32/SEG to a warp (SEG lanes per row, every row of a
+// pack from the same dependency level, so no row waits on a packmate).  The
+// same lane roles as k_ilu0_warp inside each segment; the waits are one
+// warp-uniform loop -- every segment re-polls its own pending words in the
+// same pass -- and the pivot steps run to the widest row's lower count, so
+// a warp issues each instruction once for PK rows.
+template <int COMBO, int MAXU, int SEG>
+__global__ void __launch_bounds__(kFBlock, SFG_ILU_MINB4) k_ilu0_pack(const ExecArgs A,
+                                                         const int32_t* __restrict__ uptr,
+                                                         const int32_t* __restrict__ ustep,
+                                                         const int32_t* __restrict__ usrc,
+                                                         const int32_t* __restrict__ pack_ptr,
+                                                         int32_t npack) {
+  constexpr int PK = 32 / SEG;
+  const int lane = threadIdx.x & 31;
+  const int seg = lane / SEG;
+  const int sl = lane % SEG;
+  const unsigned smask = (SEG == 32 ? FULL : ((1u << SEG) - 1u)) << (seg * SEG);
+  const bool do_fac = COMBO == 6 ? (A.phase & 1) : (A.phase & 2);
+  const bool do_solve = COMBO == 6 && (A.phase & 2);
+  const int src = COMBO == 6 ? 0 : ((A.phase & 1) ? 1 : 2);
+  const int fac_kernel = COMBO == 6 ? 1 : 2;
+  for (;;) {
+    unsigned long long w0 = 0;
+    if (lane == 0)
+      w0 = atomicAdd(A.counter, 1ull);
+    const long long pk = (long long)__shfl_sync(FULL, w0, 0);
+    if (pk >= npack)
+      break;
+    const int t0 = __ldg(pack_ptr + pk), t1 = __ldg(pack_ptr + pk + 1);
+    const int tk = t0 + seg;
+    const bool task = tk < t1;
+    int i = 0, r0 = 0, m = 0;
+    if (task) {
+      i = __ldg(A.order + A.t_begin + tk);
+      r0 = __ldg(A.ar_ptr + i);
+      m = __ldg(A.ar_ptr + i + 1) - r0;
+    }
+    const int pb = r0 + sl;
+    const bool mine = task && sl < m;
+    const int col = mine ? __ldg(A.ar_idx + pb) : 0x7fffffff;
+    const bool lower = col < i;
+    const int nl = __popc(__ballot_sync(FULL, lower) & smask); // lower lanes: sl 0 .. nl-1
+    const int nlmax = __reduce_max_sync(FULL, nl);
+    unsigned long long wx = 0;
+    const bool want_x = do_solve && lower;
+    if (want_x)
+      wx = ld_relaxed_u64(A.vout + col);
+    double acc2 = (do_solve && task) ? __ldg(A.vin + i) : 0.0;
+    if (do_fac) {
+      double acc = 0.0;
+      if (mine)
+        acc = src == 0   ? __ldg(A.ar_val + pb)
+              : src == 1 ? __dmul_rn(__dmul_rn(__ldg(A.dvec + i), __ldg(A.ar_val + pb)),
+                                     __ldg(A.dvec + col))
+                         : __ldg(A.work + pb);
+      const int dk = lower ? __ldg(A.diag + col) : -1;
+      unsigned long long wp = 0;
+      if (dk >= 0)
+        wp = ld_relaxed_u64(A.fac + dk);
+      int nu = 0, ub = 0;
+      if (mine) {
+        ub = __ldg(uptr + pb);
+        nu = __ldg(uptr + pb + 1) - ub;
+      }
+      int st[MAXU];
+      int sq[MAXU];
+      unsigned long long wu[MAXU];
+#pragma unroll
+      for (int e = 0; e < MAXU; ++e) {
+        st[e] = -1;
+        if (e < nu) {
+          st[e] = __ldg(ustep + ub + e);
+          sq[e] = __ldg(usrc + ub + e);
+        }
+      }
+#pragma unroll
+      for (int e = 0; e < MAXU; ++e)
+        if (e < nu)
+          wu[e] = ld_relaxed_u64(A.fac + sq[e]);
+      // one warp-uniform wait: every lane re-reads its own pending words in
+      // the same pass until no lane of the warp has any
+      for (;;) {
+        bool pending = (dk >= 0 && is_sent_hi(wp)) || (want_x && is_sent_hi(wx));
+#pragma unroll
+        for (int e = 0; e < MAXU; ++e)
+          pending |= e < nu && is_sent_hi(wu[e]);
+        if (!__any_sync(FULL, pending))
+          break;
+        if (dk >= 0 && is_sent_hi(wp))
+          wp = ld_relaxed_u64(A.fac + dk);
+        if (want_x && is_sent_hi(wx))
+          wx = ld_relaxed_u64(A.vout + col);
+#pragma unroll
+        for (int e = 0; e < MAXU; ++e)
+          if (e < nu && is_sent_hi(wu[e]))
+            wu[e] = ld_relaxed_u64(A.fac + sq[e]);
+      }
+      double uv[MAXU];
+#pragma unroll
+      for (int e = 0; e < MAXU; ++e)
+        uv[e] = e < nu ? __longlong_as_double((long long)wu[e]) : 0.0;
+      const double piv = dk >= 0 ? __longlong_as_double((long long)wp) : 0.0;
+      const double rcp = __drcp_rn(piv);
+      const double xk = want_x ? __longlong_as_double((long long)wx) : 0.0;
+      const int base = seg * SEG;
+#pragma unroll 2
+      for (int t = 0; t < nlmax; ++t) {
+        if (sl == t && t < nl) {
+          if (dk < 0 || piv == 0.0)
+            report_error(A.err, fac_kernel, i, col);
+          acc = div_with_rcp(acc, piv, rcp);
+        }
+        const double lik = __shfl_sync(FULL, acc, base + t);
+        if (t < nl) {
+#pragma unroll
+          for (int e = 0; e < MAXU; ++e)
+            if (st[e] == t)
+              acc = fsub_mul(acc, lik, uv[e]);
+          if (do_solve)
+            acc2 = fsub_mul(acc2, lik, __shfl_sync(FULL, xk, base + t));
+        } else if (do_solve) {
+          (void)__shfl_sync(FULL, xk, base + t);
+        }
+      }
+      if (mine)
+        publish_f64(A.fac + pb, acc);
+    } else if (do_solve) { // unit solve alone (unfused second launch)
+      double lv = 0.0, xk = 0.0;
+      if (lower) {
+        lv = poll_f64(A.fac + pb, 0);
+        xk = resolve(wx, A.vout + col, 0);
+      }
+      const double pr = __dmul_rn(lv, xk);
+      const int base = seg * SEG;
+      for (int t = 0; t < nlmax; ++t) {
+        const double v = __shfl_sync(FULL, pr, base + t);
+        if (t < nl)
+          acc2 = __dsub_rn(acc2, v);
+      }
+    }
+    if (do_solve && task && sl == 0)
+      publish_f64(A.vout + i, acc2);
+  }
+}
+
 template <typename K> void launch_warp_tasks(K kernel, const ExecArgs& a, const UpdateLists& up,
                                              cudaStream_t s) {
   const int64_t total = a.t_end - a.t_begin;
@@ -695,9 +841,38 @@ void build_ilu0_updates(const int32_t* ar_ptr, const int32_t* ar_idx, const int3
 
 int fact_warps_per_block() { return kFBlock / 32; }
 
+void build_packs(const std::vector<int64_t>& wave_ptr, int32_t seg, UpdateLists& up) {
+  up.seg = seg;
+  const int32_t pk = 32 / seg;
+  std::vector<int32_t> pp;
+  for (size_t w = 0; w + 1 < wave_ptr.size(); ++w)
+    for (int64_t a = wave_ptr[w]; a < wave_ptr[w + 1]; a += pk)
+      pp.push_back((int32_t)a);
+  pp.push_back(wave_ptr.empty() ? 0 : (int32_t)wave_ptr.back());
+  up.npack = (int32_t)pp.size() - 1;
+  up.pack_ptr.alloc((int64_t)pp.size());
+  SFG_CUDA(cudaMemcpy(up.pack_ptr.p, pp.data(), sizeof(int32_t) * pp.size(), cudaMemcpyHostToDevice));
+}
+
 bool ic0_warp_fits(const UpdateLists& up) { return up.count >= 0 && up.max_task <= 32; }
 bool ilu0_warp_fits(const UpdateLists& up) {
   return up.count >= 0 && up.max_task <= 32 && up.max_updates <= kMaxIluUpd;
+}
+
+template <typename K> void launch_pack_tasks(K kernel, const ExecArgs& a, const UpdateLists& up,
+                                             cudaStream_t s) {
+  if (up.npack <= 0)
+    return;
+  int per_sm = 0;
+  SFG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kFBlock, 0));
+  per_sm = std::max(per_sm, 1);
+  if (a.blocks_per_sm > 0 && a.blocks_per_sm < per_sm)
+    per_sm = a.blocks_per_sm;
+  int64_t blocks = ((int64_t)up.npack + (kFBlock / 32) - 1) / (kFBlock / 32);
+  blocks = std::min<int64_t>(blocks, (int64_t)per_sm * sm_count());
+  kernel<<<(unsigned)blocks, kFBlock, 0, s>>>(a, up.ptr.p, up.a.p, up.b.p, up.pack_ptr.p, up.npack);
+  count_launch();
+  SFG_CUDA(cudaGetLastError());
 }
 
 void launch_ic0_warp(int combo, const ExecArgs& a, const UpdateLists& up, cudaStream_t s) {
@@ -708,6 +883,20 @@ void launch_ic0_warp(int combo, const ExecArgs& a, const UpdateLists& up, cudaSt
 }
 
 void launch_ilu0_warp(int combo, const ExecArgs& a, const UpdateLists& up, cudaStream_t s) {
+  if (up.seg == 8 && up.max_updates <= 4) {
+    if (combo == 3)
+      launch_pack_tasks(k_ilu0_pack<3, 4, 8>, a, up, s);
+    else
+      launch_pack_tasks(k_ilu0_pack<6, 4, 8>, a, up, s);
+    return;
+  }
+  if (up.seg == 16 && up.max_updates <= 4) {
+    if (combo == 3)
+      launch_pack_tasks(k_ilu0_pack<3, 4, 16>, a, up, s);
+    else
+      launch_pack_tasks(k_ilu0_pack<6, 4, 16>, a, up, s);
+    return;
+  }
   const bool small = up.max_updates <= 4 && !getenv("SFG_ILU_MAXU8");
   if (combo == 3)
     small ? launch_warp_tasks(k_ilu0_warp<3, 4>, a, up, s) : launch_warp_tasks(k_ilu0_warp<3, 8>, a, up, s);

@@ -18,6 +18,7 @@
 #pragma once
 
 #include <cstdint>
+#include <vector>
 #include <cuda_runtime.h>
 
 #include "executor.cuh"
@@ -32,6 +33,11 @@ struct UpdateLists {
   int64_t count = 0;
   int32_t max_task = 0;    // longest column / row (lanes needed)
   int32_t max_updates = 0; // most updates of one entry
+  // packed executors (several same-level tasks per warp): SEG lanes per
+  // task, packs of 32/SEG consecutive tickets inside one wavefront
+  int32_t seg = 32;
+  int32_t npack = 0;
+  DBuf<int32_t> pack_ptr;
 };
 
 // combos 5, 7: L in CSC (lc_*) with its row view (rv_*)
@@ -46,6 +52,9 @@ void build_ilu0_updates(const int32_t* ar_ptr, const int32_t* ar_idx, const int3
 // column / row entry; ILU0 keeps each entry's updates in registers).
 // warps in one block of the factorization executors (occupancy sizing)
 int fact_warps_per_block();
+// Packs of 32/seg consecutive tickets that never cross a wavefront boundary
+// (wave_ptr over the ticket order); sets up.seg / npack / pack_ptr.
+void build_packs(const std::vector<int64_t>& wave_ptr, int32_t seg, UpdateLists& up);
 bool ic0_warp_fits(const UpdateLists& up);
 bool ilu0_warp_fits(const UpdateLists& up);
 

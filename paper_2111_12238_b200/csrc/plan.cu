@@ -758,6 +758,14 @@ void do_inspect(sfg_plan* P) {
   } else if (!legacy && (combo == 6 || combo == 3)) {
     build_ilu0_updates(P->ar_ptr.p, P->ar_idx.p, P->diag.p, n, P->nnzF, P->upd, s);
     P->use_warpfac = ilu0_warp_fits(P->upd);
+    // rows of at most 8 / 16 entries: 4 / 2 same-level rows per warp
+    const char* pk = getenv("SFG_ILU_PACK");
+    if (P->use_warpfac && P->upd.max_updates <= 4 && !(pk && std::string(pk) == "0")) {
+      if (P->upd.max_task <= 8 && !(pk && std::string(pk) == "16"))
+        build_packs(P->wave_ptr, 8, P->upd);
+      else if (P->upd.max_task <= 16)
+        build_packs(P->wave_ptr, 16, P->upd);
+    }
   }
   if (!P->use_warpfac)
     P->upd = UpdateLists{};

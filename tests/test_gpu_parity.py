@@ -414,6 +414,27 @@ def test_mline_executor_vs_oracle(orc, monkeypatch, executor, nsys, rows):
             assert np.array_equal(got[s], want)
 
 
+@pytest.mark.parametrize("pack", ("0", "8", "16"))
+@pytest.mark.parametrize("combo", (3, 6))
+def test_ilu0_packing_modes(orc, golden, monkeypatch, pack, combo):
+    """The ILU0 executor with 1, 2 or 4 same-level rows per warp
+    (SFG_ILU_PACK 0 / 16 / 8): golden matrices and the C3 matrix, bit-exact,
+    fused and unfused."""
+    monkeypatch.setenv("SFG_ILU_PACK", pack)
+    for name in GOLDEN_MATS:
+        st = sf.make_state(combo, as_sf(golden_matrix(golden, name)), seed=7)
+        want = golden[f"{name}/c{combo}/outputs"]
+        st.execute_fused()
+        assert np.array_equal(st.collect_outputs(), want)
+        st.execute_unfused()
+        assert np.array_equal(st.collect_outputs(), want)
+    M = sf.config_matrix(3, size=40)
+    want = orc.run_sequential(combo, Csc(M.n, M.colptr, M.rowidx, M.values), 7)
+    st = sf.make_state(combo, M, seed=7)
+    st.execute_fused()
+    assert np.array_equal(st.collect_outputs(), want)
+
+
 # ---- the GPU schedule checked by the reference's own validator ------------------
 def _validated_by_reference(st, combo, Mo):
     from oracle.oracle import Reference
