@@ -294,6 +294,8 @@ class Reference:
         L.ref_validate_partitioning.argtypes = [vp, C.c_int32, _i64p, _i64p,
                                                 C.POINTER(C.c_uint8), _i32p, C.c_char_p, C.c_int]
         L.ref_validate_partitioning.restype = C.c_int64
+        L.ref_replay_partitioning.argtypes = [vp, C.c_int32, _i64p, _i64p, C.POINTER(C.c_uint8), _i32p,
+                                              C.c_uint64, _f64p, C.c_int64, _i32p, C.c_char_p, C.c_int]
         L.ref_read_mm.argtypes = [C.c_char_p, C.c_char_p, C.c_int]
         L.ref_read_mm.restype = vp
         L.ref_fwd_bwd.argtypes = [C.c_int32, _i32p, _i32p, _f64p, _f64p, _f64p, _i32p,
@@ -589,6 +591,25 @@ class RefState:
             self.h, len(sp) - 1, _p(sp, _i64p), _p(wp, _i64p),
             tg.ctypes.data_as(C.POINTER(C.c_uint8)), _p(it, _i32p), msg, 512)
         return int(nbad), msg.value.decode()
+
+    def replay_partitioning(self, s_ptr, w_ptr, tags, iters, seed: int) -> np.ndarray:
+        """replay_schedule (executor.hpp:518-553) of an external partitioning
+        in flat form; returns collect_outputs."""
+        sp = np.ascontiguousarray(s_ptr, np.int64)
+        wp = np.ascontiguousarray(w_ptr, np.int64)
+        tg = np.ascontiguousarray(tags, np.uint8)
+        it = np.ascontiguousarray(iters, np.int32)
+        n = int(self.ref.lib.ref_output_len(self.h))
+        out = np.empty(max(n, 1), np.float64)
+        ei = C.c_int32(-1)
+        msg = C.create_string_buffer(512)
+        rc = self.ref.lib.ref_replay_partitioning(
+            self.h, len(sp) - 1, _p(sp, _i64p), _p(wp, _i64p),
+            tg.ctypes.data_as(C.POINTER(C.c_uint8)), _p(it, _i32p), seed, _p(out, _f64p), len(out),
+            C.byref(ei), msg, 512)
+        if rc:
+            raise RuntimeError(msg.value.decode())
+        return out[:n]
 
     def bench(self, executor: int, nthreads: int, warmups: int = 2, repeats: int = 5):
         """Returns (per-repeat seconds, inspector seconds, s-partitions)."""

@@ -391,6 +391,38 @@ int64_t ref_validate_partitioning(void* s, int32_t nspart, const int64_t* s_ptr,
   return (int64_t)bad.size();
 }
 
+// replay_schedule (executor.hpp:518-553) of an external partitioning in flat
+// form: one thread, w-partitions of each s-partition interleaved in a seeded
+// random order, then collect_outputs into out.  Returns the ref_execute codes.
+int ref_replay_partitioning(void* s, int32_t nspart, const int64_t* s_ptr, const int64_t* w_ptr,
+                            const uint8_t* tags, const int32_t* iters, uint64_t seed, double* out,
+                            int64_t cap, int32_t* err_index, char* msg, int ml) {
+  auto* st = static_cast<KernelState*>(s);
+  return guarded(
+      [&] {
+        FusedPartitioning V;
+        V.fusion = true;
+        V.n1 = V.n2 = st->n;
+        V.spartitions.resize((std::size_t)nspart);
+        for (int32_t k = 0; k < nspart; ++k)
+          for (int64_t w = s_ptr[k]; w < s_ptr[k + 1]; ++w) {
+            std::vector<FusedEntry> es;
+            for (int64_t e = w_ptr[w]; e < w_ptr[w + 1]; ++e)
+              es.push_back(FusedEntry{tags[e], iters[e], false});
+            V.spartitions[(std::size_t)k].push_back(std::move(es));
+          }
+        std::vector<std::string> dups;
+        replay_schedule(V, *st, seed, true, &dups);
+        if (!dups.empty())
+          throw std::logic_error(dups.front());
+        const std::vector<double> o = collect_outputs(*st);
+        if ((int64_t)o.size() > cap)
+          throw std::invalid_argument("output buffer too small");
+        std::copy(o.begin(), o.end(), out);
+      },
+      err_index, msg, ml);
+}
+
 // read_matrix_market (matrix_market.hpp:59-121); nullptr + message on error.
 void* ref_read_mm(const char* path, char* msg, int ml) {
   try {

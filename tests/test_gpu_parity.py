@@ -447,6 +447,24 @@ def _validated_by_reference(st, combo, Mo):
 
 
 @pytest.mark.parametrize("name", GOLDEN_MATS)
+@pytest.mark.parametrize("combo", (1, 2, 3, 5, 6, 7))
+def test_partitioning_replayed_by_reference(golden, name, combo):
+    """replay_schedule (executor.hpp:518-553): the reference runs the GPU's
+    exported partitioning with its w-partitions interleaved in random orders;
+    every replay reproduces the reference's sequential outputs (combo 4's CSC
+    scatter is order-dependent and is checked by the validator only)."""
+    from oracle.oracle import Reference
+    Mo = golden_matrix(golden, name)
+    st = sf.make_state(combo, as_sf(Mo)).inspect()
+    part = st.partitioning()
+    rs = Reference().state(combo, Mo, 7)
+    want = golden[f"{name}/c{combo}/outputs"]
+    for seed in (1, 2, 3):
+        got = rs.replay_partitioning(part.s_ptr, part.w_ptr, part.tags, part.iters, seed)
+        assert np.array_equal(got, want)
+
+
+@pytest.mark.parametrize("name", GOLDEN_MATS)
 @pytest.mark.parametrize("combo", (1, 2, 3, 4, 5, 6, 7))
 def test_partitioning_valid_for_reference(golden, name, combo):
     # validate_fused_partitioning (msp.hpp:1108-1237): coverage, order inside
