@@ -88,7 +88,6 @@ struct ChainArgs {
   int64_t bwd_reset_words = 0;
   int32_t bwd_reset_items = 0;
   unsigned long long* reset_done = nullptr;
-  unsigned poll_ns = 0;   // lockstep executor: sleep before a re-poll round (0 = spin)
   unsigned bwd_gate = 500; // ns a backward chain's first lane sleeps per check (0 = off)
   // optional timeline trace: per (work item, tile) {claim, partial done,
   // carry done} in %globaltimer ns (diagnostics only; null in production)
@@ -111,13 +110,5 @@ inline int32_t chain_G(int32_t S, int32_t override_rows = 0) {
 inline int32_t chain_CS(int32_t) { return 1; }
 
 void launch_chain(const ChainArgs& a, cudaStream_t s);
-
-// Lockstep executor (lock.cu): batches of 32/S chains of one level per warp,
-// one row per chain per step; layouts built with G = 1, CS = 32/S.  A row may
-// carry at most kLockTerms external (non-carry) dependencies.
-constexpr int kLockTerms = 12;
-int32_t lock_max_terms(const int32_t* ptr, int32_t n, int dir, const ChainLayout& L,
-                       cudaStream_t s);
-void launch_lock(const ChainArgs& a, cudaStream_t s);
 
 } // namespace sfg

@@ -74,7 +74,6 @@ struct sfg_plan {
   // chain executor (combos 1, 4, 8); the level-set kernel stays available
   // as SFG_EXECUTOR=levels for ablations
   bool use_chain = false;
-  bool use_lock = false; // lockstep batches (lock.cu): combo 8, nsys >= 2
   ChainLayout ch_f, ch_b;
   DBuf<int32_t> tail_ptr, tail_rows;
   std::vector<int32_t> row_maxcol; // (unused by the chain path; kept for stats)
@@ -781,22 +780,9 @@ void do_inspect(sfg_plan* P) {
     int32_t max_len = 4096;
     if (const char* e = getenv("SFG_CHAIN_MAX"))
       max_len = atoi(e);
-    // batched fwd -> bwd: the lockstep executor (lock.cu), 32/nsys chains of
-    // one level per warp, when no row has more than kLockTerms external
-    // dependencies; SFG_EXECUTOR=chain keeps one chain per warp
-    const bool want_lock = combo == 8 && P->nsys >= 2 && P->nsys <= 32 &&
-                           (P->nsys & (P->nsys - 1)) == 0 && !(ex && std::string(ex) == "chain");
-    if (want_lock) {
-      build_chains(P->lr_ptr.p, P->lr_idx.p, n, +1, 1, 32 / P->nsys, max_len, P->ch_f, s);
-      build_chains(P->lt_ptr.p, P->lt_idx.p, n, -1, 1, 32 / P->nsys, max_len, P->ch_b, s);
-      P->use_lock = lock_max_terms(P->lr_ptr.p, n, +1, P->ch_f, s) <= kLockTerms &&
-                    lock_max_terms(P->lt_ptr.p, n, -1, P->ch_b, s) <= kLockTerms;
-    }
-    if (!P->use_lock) {
-      build_chains(P->lr_ptr.p, P->lr_idx.p, n, +1, G, CS, max_len, P->ch_f, s);
-      if (combo == 8)
-        build_chains(P->lt_ptr.p, P->lt_idx.p, n, -1, G, CS, max_len, P->ch_b, s);
-    }
+    build_chains(P->lr_ptr.p, P->lr_idx.p, n, +1, G, CS, max_len, P->ch_f, s);
+    if (combo == 8)
+      build_chains(P->lt_ptr.p, P->lt_idx.p, n, -1, G, CS, max_len, P->ch_b, s);
     if (combo == 4)
       build_tails(P->ch_f, P->ar_ptr.p, P->ar_idx.p, n, P->tail_ptr, P->tail_rows, s);
     if (getenv("SFG_TRACE")) {
@@ -900,8 +886,6 @@ ChainArgs chain_args(sfg_plan* P) {
   a.tail_rows = P->tail_rows.p;
   if (const char* e = getenv("SFG_BWD_GATE"))
     a.bwd_gate = (unsigned)atoi(e);
-  if (const char* e = getenv("SFG_LOCK_SLEEP"))
-    a.poll_ns = (unsigned)atoi(e);
   a.ar_ptr = P->ar_ptr.p;
   a.ar_idx = P->ar_idx.p;
   a.ar_val = P->ar_val.p;
@@ -1223,10 +1207,7 @@ void exec_fused_impl(sfg_plan* P, cudaEvent_t kb, cudaEvent_t ke) {
     }
     b.seg_begin = 0;
     b.seg_end = P->ch_f.nbatch + (P->combo == 8 ? P->ch_b.nbatch : 0);
-    if (P->use_lock)
-      launch_lock(b, P->stream);
-    else
-      launch_chain(b, P->stream);
+    launch_chain(b, P->stream);
   } else {
     ExecArgs a = exec_args(P);
     a.phase = 3;
@@ -1323,10 +1304,7 @@ void exec_unfused_impl(sfg_plan* P, cudaEvent_t kb, cudaEvent_t ke, int which = 
       b.phase = 1;
       b.seg_begin = 0;
       b.seg_end = P->ch_f.nbatch;
-      if (P->use_lock)
-        launch_lock(b, P->stream);
-      else
-        launch_chain(b, P->stream);
+      launch_chain(b, P->stream);
     }
     if (k2) {
       FillRegion r2[1];
@@ -1341,10 +1319,7 @@ void exec_unfused_impl(sfg_plan* P, cudaEvent_t kb, cudaEvent_t ke, int which = 
         b.seg_begin = P->ch_f.nbatch;
         b.seg_end = P->ch_f.nbatch + P->ch_b.nbatch;
       }
-      if (P->use_lock)
-        launch_lock(b, P->stream);
-      else
-        launch_chain(b, P->stream);
+      launch_chain(b, P->stream);
     }
     SFG_CUDA(cudaEventRecord(ke, P->stream));
     return;
