@@ -248,6 +248,19 @@ def copy_bound(h2d_bytes: int, d2h_bytes: int, device: int, reps: int = 5):
         return {"error": str(e)[:200]}
 
 
+def workload_config(cfg: int, combo: int, n: int, nnzA: int, nnzL: int, S: int, world: int):
+    """The `config` object of a bench line: the same dict for our arm and for
+    the reference arm, so the driver can match them key by key."""
+    name = CONFIG_NAME[cfg]
+    if cfg == 5 and combo == 1:
+        name = name.replace("bwd L^T", "fwd L (combo 1 parity mode)")
+    return {"workload": name, "baseline_config": cfg, "combo": combo, "n": n, "nnz_A": nnzA,
+            "nnz_L": nnzL, "systems_per_gpu": S, "global_systems": S * world,
+            "l2": ("inputs larger than L2 (L values+indices %.2f GB/GPU > 126 MB)"
+                   % (S * 12 * nnzL / 1e9)) if cfg == 5 else "see DESIGN.md",
+            "parallelism": f"dp{world} (independent systems, no collective)"}
+
+
 def lower_nnz(M) -> int:
     cols = np.repeat(np.arange(M.n, dtype=np.int64), np.diff(M.colptr))
     return int(np.count_nonzero(M.rowidx >= cols))
@@ -494,13 +507,7 @@ def run_ours(args, D: Dist):
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
         "scaling": scaling_kind(args, cfg, D), "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
-        "config": {"workload": CONFIG_NAME[cfg] if not (cfg == 5 and combo == 1)
-                   else CONFIG_NAME[5].replace("bwd L^T", "fwd L (combo 1 parity mode)"),
-                   "baseline_config": cfg, "combo": combo, "n": M.n, "nnz_A": M.nnz,
-                   "nnz_L": nnzL, "systems_per_gpu": S, "global_systems": S * D.world,
-                   "l2": "inputs larger than L2 (L values+indices %.2f GB/GPU > 126 MB)"
-                   % (S * 12 * nnzL / 1e9) if cfg == 5 else "see DESIGN.md",
-                   "parallelism": f"dp{D.world} (independent systems, no collective)"},
+        "config": workload_config(cfg, combo, M.n, M.nnz, nnzL, S, D.world),
         "parity": parity,
         "gpu_launches": launches,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
@@ -795,8 +802,7 @@ def run_reference(args, D: Dist):
                   "the reference has no fwd->bwd pair), sum of executor wall times; "
                   f"{args.steps} steps after {warm} warm-ups; schedules built once "
                   f"({insp:.1f}s, excluded)")
-        cfgd = {"workload": CONFIG_NAME[5], "baseline_config": 5, "combo": 8, "n": M.n,
-                "nnz_A": M.nnz, "global_systems": nsys}
+        cfgd = workload_config(5, 8, M.n, M.nnz, lower_nnz(M), nsys // D.world, D.world)
     else:
         M, _, vin = ref_inputs(ref, cfg, args.size)
         r = reference_fused(cfg, M, vin, T, warmups=warm, repeats=args.steps)
@@ -805,8 +811,7 @@ def run_reference(args, D: Dist):
         combo, insp, nsp = r["combo"], r["inspector_s"], r["s_partitions"]
         sample = (f"reference execute_fused, T={T} host threads, 1 execution per step "
                   f"({args.steps} steps after {warm} warm-ups; msp inspector {insp:.1f}s excluded)")
-        cfgd = {"workload": CONFIG_NAME[cfg], "baseline_config": cfg, "combo": combo, "n": M.n,
-                "nnz_A": M.nnz, "global_systems": 1}
+        cfgd = workload_config(cfg, combo, M.n, M.nnz, lower_nnz(M), 1, D.world)
     assert "paper_2111_12238_b200" not in sys.modules, "the reference arm must not load our package"
     return {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": D.world,
