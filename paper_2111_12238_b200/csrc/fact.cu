@@ -24,8 +24,9 @@
 
 #ifndef SFG_IC5_CHU
 // IC0 combo 5: update slots per batch.  Four (72 registers, 3 blocks per SM)
-// instead of eight (116 registers, 2 blocks): C2 0.478 -> 0.444 ms
-#define SFG_IC5_CHU 4
+// instead of eight (116 registers, 2 blocks): C2 0.478 -> 0.444 ms; three
+// slots compiled for 4 blocks per SM: 0.358 -> 0.348 ms (two: 0.378 ms)
+#define SFG_IC5_CHU 3
 #endif
 #ifndef SFG_IC7_CHU
 #define SFG_IC7_CHU 4 // IC0 combo 7: update slots per batch (8: 9.53 ms, 4: 9.18 ms on C4)
@@ -34,7 +35,7 @@
 #define SFG_IC7_MINB 1 // blocks per SM k_ic0_warp<7> is compiled for (A/B builds)
 #endif
 #ifndef SFG_IC5_MINB
-#define SFG_IC5_MINB 1 // blocks per SM k_ic0_warp<5> is compiled for (A/B builds)
+#define SFG_IC5_MINB 4 // blocks per SM k_ic0_warp<5> is compiled for (A/B builds)
 #endif
 
 #ifndef SFG_ILU_MINB4
@@ -279,6 +280,8 @@ __global__ void __launch_bounds__(kFBlock, COMBO == 5 ? SFG_IC5_MINB : SFG_IC7_M
     // factorization of column k
     unsigned long long wl = 0, wx = 0;
     int ql = -1, qx = -1;
+    // the right-hand side of the solve row, in flight during the factorization too
+    const double bk = do_solve ? __ldg(A.vin + k) : 0.0;
     if (do_solve && q0 + lane < q1) {
       ql = __ldg(A.rv_pos + q0 + lane);
       qx = __ldg(A.rv_col + q0 + lane);
@@ -401,7 +404,7 @@ __global__ void __launch_bounds__(kFBlock, COMBO == 5 ? SFG_IC5_MINB : SFG_IC7_M
       lkk = do_solve ? poll_f64(A.fac + c0, cap) : 0.0;
     }
     if (do_solve) {
-      double acc2 = __ldg(A.vin + k);
+      double acc2 = bk;
       for (int qb = q0; qb < q1; qb += 32) {
         double lv = 0.0, xv = 0.0;
         if (qb + lane < q1) {
