@@ -87,6 +87,11 @@ def test_reference_arm_matches_our_config_and_skips_the_package():
     import bench
     assert d["config"]["workload"] == bench.CONFIG_NAME[5]
     assert d["config"]["combo"] == 8 and d["config"]["global_systems"] == bench.GLOBAL_BATCH
+    # the same object, key by key, as our arm prints for this workload
+    n = 10 ** 3
+    ours = bench.workload_config(5, 8, n, d["config"]["nnz_A"], d["config"]["nnz_L"],
+                                 bench.GLOBAL_BATCH, 1)
+    assert d["config"] == ours
 
 
 def test_warmup_floor():
