@@ -7,6 +7,8 @@
 // separately rounded multiply and subtract, IEEE square root, and divisions
 // that are IEEE-exact (div_with_rcp falls back to the IEEE division outside
 // its proven range).
+#include <cstdlib>
+
 #include <cub/cub.cuh>
 
 #include "common.cuh"
@@ -453,6 +455,190 @@ __global__ void __launch_bounds__(kFBlock, COMBO == 5 ? SFG_IC5_MINB : SFG_IC7_M
   }
 }
 
+// Per-ticket task record of the IC0 executors, in claim order: {column k,
+// lc_ptr[k], lc_ptr[k+1], rv_ptr[k]}, {rv_ptr[k+1], -, -, -}.  One load by
+// ticket number replaces the order -> pointer chain at the start of a task.
+__global__ void k_ic0_task_records(const int32_t* __restrict__ order,
+                                   const int32_t* __restrict__ lc_ptr,
+                                   const int32_t* __restrict__ rv_ptr, int64_t ntask,
+                                   int4* __restrict__ rec) {
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < ntask;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int k = order[t];
+    rec[2 * t] = make_int4(k, lc_ptr[k], lc_ptr[k + 1], rv_ptr[k]);
+    rec[2 * t + 1] = make_int4(rv_ptr[k + 1], 0, 0, 0);
+  }
+}
+
+// Fused IC0 -> solve (combo 5, both kernels in one launch) with the operands
+// of the NEXT task loaded during the current one.  A warp holds three
+// tickets in claim order: the task it runs, the next one (its record loaded
+// a task ago, its per-lane operands -- column values, update-list bounds, the
+// solve row's entries, the right-hand side -- loaded between this task's
+// factorization and its solve) and a third whose record is in flight.  A
+// task then starts with its update-list and factor-word loads instead of
+// five dependent round trips.  Tickets are claimed in increasing order and
+// run in that order, so the smallest unfinished ticket is always running:
+// deadlock-free like k_ic0_warp.  Arithmetic and error reporting are
+// k_ic0_warp<5>'s.
+struct IcLane {
+  double acc, bk;
+  int u0, u1, ql, qx;
+};
+
+template <int CHU>
+__global__ void __launch_bounds__(kFBlock, 3) k_ic0_pipe(const ExecArgs A,
+                                                         const int32_t* __restrict__ uptr,
+                                                         const int32_t* __restrict__ usrc,
+                                                         const int32_t* __restrict__ ulkj,
+                                                         const int4* __restrict__ trec) {
+  const int lane = threadIdx.x & 31;
+  const int64_t total = A.t_end - A.t_begin;
+  auto claim = [&]() {
+    unsigned long long nb = 0;
+    if (lane == 0)
+      nb = atomicAdd(A.counter, 1ull);
+    return (long long)__shfl_sync(FULL, nb, 0);
+  };
+  auto load_rec = [&](long long t, int4& a, int4& b) {
+    if (t < total) {
+      a = __ldg(trec + 2 * (A.t_begin + t));
+      b = __ldg(trec + 2 * (A.t_begin + t) + 1);
+    }
+  };
+  auto load_lane = [&](const int4& a, const int4& b, IcLane& L) {
+    const int c0 = a.y, m = a.z - a.y, q0 = a.w, q1 = b.x;
+    L.acc = 0.0;
+    L.u0 = L.u1 = 0;
+    L.ql = L.qx = -1;
+    if (lane < m) {
+      L.acc = __ldg(A.lc_val + c0 + lane);
+      L.u0 = __ldg(uptr + c0 + lane);
+      L.u1 = __ldg(uptr + c0 + lane + 1);
+    }
+    if (q0 + lane < q1) {
+      L.ql = __ldg(A.rv_pos + q0 + lane);
+      L.qx = __ldg(A.rv_col + q0 + lane);
+    }
+    L.bk = __ldg(A.vin + a.x);
+  };
+  long long t0 = claim(), t1 = claim();
+  int4 ha0 = make_int4(0, 0, 0, 0), hb0 = ha0, ha1 = ha0, hb1 = ha0;
+  load_rec(t0, ha0, hb0);
+  load_rec(t1, ha1, hb1);
+  IcLane L0{0.0, 0.0, 0, 0, -1, -1}, L1 = L0;
+  if (t0 < total)
+    load_lane(ha0, hb0, L0);
+  while (t0 < total) {
+    unsigned long long nb = 0;
+    if (lane == 0)
+      nb = atomicAdd(A.counter, 1ull);
+    const int k = ha0.x, c0 = ha0.y, m = ha0.z - ha0.y, q0 = ha0.w, q1 = hb0.x;
+    // the solve's first 32 operands L(k,j), x_j: in flight during the factorization
+    int ql = L0.ql, qx = L0.qx;
+    unsigned long long wl = 0, wx = 0;
+    if (ql >= 0) {
+      wl = ld_relaxed_u64(A.fac + ql);
+      wx = ld_relaxed_u64(A.vout + qx);
+    }
+    const int pa = c0 + lane;
+    double acc = L0.acc;
+    const int u0 = L0.u0, u1 = L0.u1;
+    for (int u = u0; u < u1; u += CHU) {
+      const int cnt = min(CHU, u1 - u);
+      int ps[CHU], pl[CHU];
+      unsigned long long ws[CHU], wk[CHU];
+#pragma unroll
+      for (int e = 0; e < CHU; ++e)
+        if (e < cnt) {
+          ps[e] = __ldg(usrc + u + e);
+          pl[e] = __ldg(ulkj + u + e);
+        }
+#pragma unroll
+      for (int e = 0; e < CHU; ++e)
+        if (e < cnt) {
+          ws[e] = ld_relaxed_u64(A.fac + ps[e]);
+          wk[e] = ld_relaxed_u64(A.fac + pl[e]);
+        }
+      for (;;) {
+        bool pending = false;
+#pragma unroll
+        for (int e = 0; e < CHU; ++e)
+          pending |= e < cnt && (is_sent_hi(ws[e]) || is_sent_hi(wk[e]));
+        if (!pending)
+          break;
+#pragma unroll
+        for (int e = 0; e < CHU; ++e)
+          if (e < cnt) {
+            if (is_sent_hi(ws[e]))
+              ws[e] = ld_relaxed_u64(A.fac + ps[e]);
+            if (is_sent_hi(wk[e]))
+              wk[e] = ld_relaxed_u64(A.fac + pl[e]);
+          }
+      }
+#pragma unroll
+      for (int e = 0; e < CHU; ++e)
+        if (e < cnt)
+          acc = fsub_mul(acc, __longlong_as_double((long long)wk[e]),
+                         __longlong_as_double((long long)ws[e]));
+    }
+    double l0 = 0.0;
+    if (lane == 0) {
+      if (acc <= 0.0)
+        report_error(A.err, 1, k, k);
+      l0 = __dsqrt_rn(acc);
+    }
+    const double lkk = __shfl_sync(FULL, l0, 0);
+    if (lane < m)
+      publish_f64(A.fac + pa, lane == 0 ? lkk : __ddiv_rn(acc, lkk));
+    // the next task's per-lane operands (its record arrived a task ago)
+    if (t1 < total)
+      load_lane(ha1, hb1, L1);
+    // solve row k (trsv_csc_row, kernels.hpp:200-210)
+    double acc2 = L0.bk;
+    for (int qb = q0; qb < q1; qb += 32) {
+      double lv = 0.0, xv = 0.0;
+      if (qb + lane < q1) {
+        if (qb != q0) {
+          ql = __ldg(A.rv_pos + qb + lane);
+          qx = __ldg(A.rv_col + qb + lane);
+          wl = ld_relaxed_u64(A.fac + ql);
+          wx = ld_relaxed_u64(A.vout + qx);
+        }
+        // L(k,j) and x_j come from the same task j: await them together
+        while (is_sent_hi(wl) || is_sent_hi(wx)) {
+          if (is_sent_hi(wl))
+            wl = ld_relaxed_u64(A.fac + ql);
+          if (is_sent_hi(wx))
+            wx = ld_relaxed_u64(A.vout + qx);
+        }
+        lv = __longlong_as_double((long long)wl);
+        xv = __longlong_as_double((long long)wx);
+      }
+      const int cnt = min(32, q1 - qb);
+      const double pr = __dmul_rn(lv, xv);
+#if SFG_IC_UNROLL
+      constexpr int kUnrollS = SFG_IC_UNROLL;
+#pragma unroll kUnrollS
+#endif
+      for (int t = 0; t < cnt; ++t)
+        acc2 = __dsub_rn(acc2, __shfl_sync(FULL, pr, t));
+    }
+    if (lane == 0) {
+      if (lkk == 0.0)
+        report_error(A.err, 2, k, k);
+      publish_f64(A.vout + k, __ddiv_rn(acc2, lkk));
+    }
+    // rotate the ticket queue
+    t0 = t1;
+    ha0 = ha1;
+    hb0 = hb1;
+    L0 = L1;
+    t1 = (long long)__shfl_sync(FULL, nb, 0);
+    load_rec(t1, ha1, hb1);
+  }
+}
+
 // IKJ ILU0 row i (ilu0_row, kernels.hpp:246-272) fused with the unit-lower
 // solve y_i (trsv_csr_unit_row, kernels.hpp:184-196).  Pivot step t is the
 // t-th lower entry k_t of row i: lane t forms l_{i,k_t} = a_{i,k_t} / u_{k_t k_t}
@@ -879,6 +1065,33 @@ template <typename K> void launch_pack_tasks(K kernel, const ExecArgs& a, const 
 }
 
 void launch_ic0_warp(int combo, const ExecArgs& a, const UpdateLists& up, cudaStream_t s) {
+  static const bool pipe_off = getenv("SFG_IC5_PIPE") && atoi(getenv("SFG_IC5_PIPE")) == 0;
+  if (combo == 5 && a.phase == 3 && !a.ftrace && !pipe_off && a.t_begin == 0) {
+    // the fused launch: task records in claim order, operands one task ahead
+    const int64_t total = a.t_end - a.t_begin;
+    if (total <= 0)
+      return;
+    if (up.trec.n < 8 * total) {
+      up.trec.alloc(8 * total);
+      k_ic0_task_records<<<grid_n(total), kFBlock, 0, s>>>(a.order, a.lc_ptr, a.rv_ptr, total,
+                                                          reinterpret_cast<int4*>(up.trec.p));
+      count_launch();
+      SFG_CUDA(cudaGetLastError());
+    }
+    auto kernel = k_ic0_pipe<SFG_IC5_CHU>;
+    int per_sm = 0;
+    SFG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kFBlock, 0));
+    per_sm = std::max(per_sm, 1);
+    if (a.blocks_per_sm > 0 && a.blocks_per_sm < per_sm)
+      per_sm = a.blocks_per_sm;
+    int64_t blocks = (total + (kFBlock / 32) - 1) / (kFBlock / 32);
+    blocks = std::min<int64_t>(blocks, (int64_t)per_sm * sm_count());
+    kernel<<<(unsigned)blocks, kFBlock, 0, s>>>(a, up.ptr.p, up.a.p, up.b.p,
+                                                reinterpret_cast<const int4*>(up.trec.p));
+    count_launch();
+    SFG_CUDA(cudaGetLastError());
+    return;
+  }
   if (combo == 5)
     launch_warp_tasks(k_ic0_warp<5>, a, up, s);
   else

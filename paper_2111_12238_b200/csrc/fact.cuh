@@ -38,6 +38,9 @@ struct UpdateLists {
   int32_t seg = 32;
   int32_t npack = 0;
   DBuf<int32_t> pack_ptr;
+  // IC0 task records in claim order (8 ints per ticket), built at the first
+  // fused launch of a combo-5 plan (k_ic0_pipe)
+  mutable DBuf<int32_t> trec;
 };
 
 // combos 5, 7: L in CSC (lc_*) with its row view (rv_*)
