@@ -208,7 +208,7 @@ def kernel_name(cfg: int, combo: int, S: int) -> str:
         return {4: "k_mline1 (fwd L + SpMV row blocks)", 2: "k_mline1 (SpMV blocks + fwd L)"}.get(
             combo, f"k_mline1 (combo {combo})")
     return {8: f"k_chain_sm<{S},{G},12,8> (fwd L + bwd L^T)", 1: f"k_chain_sm<{S},{G},12,1> (fwd L + fwd L)",
-            5: "k_ic0_warp<5>", 6: "k_ilu0_pack<6,4,8> (4 rows per warp)",
+            5: "k_ic0_pipe (task records, operands one task ahead)", 6: "k_ilu0_pack<6,4,8> (4 rows per warp)",
             3: "k_ilu0_pack<3,4,8> (4 rows per warp)",
             7: "k_ic0_warp<7>"}.get(combo, f"combo {combo} executor")
 
