@@ -51,6 +51,11 @@ for part, sl in (("fwd", slice(0, nf)), ("bwd", slice(nf, items))):
     print("  per-level lag of first-tile end: median %.2f us, mean %.2f" % (np.median(lag), lag.mean()))
     lag = np.diff(rows[:, 4])
     print("  per-level lag of tile-16 end: median %.2f us, mean %.2f" % (np.median(lag), lag.mean()))
+    # by tile skew class (level mod 4): a level whose skew wraps to 0 needs its producers' NEXT tile
+    lv = rows[1:, 0].astype(int)
+    for col, nm in ((2, "first-tile"), (4, "tile-16"), (5, "last-tile")):
+        d = np.diff(rows[:, col])
+        print("  lag of %s end by level mod 4:" % nm, [round(float(np.median(d[lv % 4 == m])), 2) for m in range(4)])
     per = np.concatenate([np.diff(E[i, :nt[i]]) for i in range(0, E.shape[0], 7)])
     print("  in-chain tile period us p10/50/90", np.percentile(per, [10, 50, 90]).round(2))
     # split of one tile: gap (previous tile end -> stage-D entry: stages A-C and the copy wait),
