@@ -1,7 +1,10 @@
 // mline.cu -- inspector and executor of the multi-chain warp scheme (see
 // mline.cuh).
 #ifndef SFG_ML1_UNROLL
-#define SFG_ML1_UNROLL 4 // unroll factor of k_mline1's step loop (C1 0.618 -> 0.587 ms; 2: 0.596)
+// unroll factor of k_mline1's step loop: with ring sizes that are powers of
+// two, 8 turns every ring index into a compile-time constant (C1 kernel
+// 0.589 -> 0.576 ms from the ring sizes, -> 0.535 ms at 8; 4: 0.576, 16: 0.599)
+#define SFG_ML1_UNROLL 8
 #endif
 #include "common.cuh"
 #include "mline.cuh"
@@ -572,8 +575,9 @@ __global__ void __launch_bounds__(kMThreads) k_mline(const MLineArgs A) {
 // completes its row from shared memory (ring for in-group dependencies).
 constexpr int kXA1 = 2;        // gathers run kXA1 steps ahead
 constexpr int kRA1 = 2 * kXA1; // records run kRA1 steps ahead
-constexpr int kQ1 = kRA1 + 1;  // record slots: steps i .. i+kRA1
-constexpr int kX1 = kXA1 + 1;  // gathered-word slots: steps i .. i+kXA1
+constexpr int kQ1 = 8;         // record slots (a power of two >= kRA1 + 1): steps i .. i+kRA1
+constexpr int kX1 = 4;         // gathered-word slots (a power of two >= kXA1 + 1): steps i .. i+kXA1
+static_assert(kQ1 >= kRA1 + 1 && kX1 >= kXA1 + 1 && (kQ1 & (kQ1 - 1)) == 0 && (kX1 & (kX1 - 1)) == 0, "ring sizes");
 template <int CH> struct alignas(16) Ml1Warp {
   double v[kQ1][32][CH + 4]; // deps, carry coefficient, diagonal, its reciprocal, pad
   int32_t cd[kQ1][32][CH];
@@ -583,9 +587,13 @@ template <int CH> struct alignas(16) Ml1Warp {
   double ring[kRing][32];
 };
 
+#ifndef SFG_ML1_TRACE
+#define SFG_ML1_TRACE 0 // 1: k_mline1 records its timeline when SFG_TRACE is set (diagnostic builds)
+#endif
 template <int CH>
 __global__ void __launch_bounds__(kMThreads) k_mline1(const MLineArgs A) {
   static_assert(CH == 2 || CH == 4, "record widths of 32 or 48 bytes");
+  const bool tracing = SFG_ML1_TRACE && A.trace;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Ml1Warp<CH>& W = reinterpret_cast<Ml1Warp<CH>*>(smem_raw)[threadIdx.x >> 5];
   const int lane = threadIdx.x & 31;
@@ -649,7 +657,7 @@ __global__ void __launch_bounds__(kMThreads) k_mline1(const MLineArgs A) {
     double carry = 0.0;
     bool started = false;
     unsigned long long tr_claim = 0, tr_first = 0, poll_cyc = 0, d_cyc = 0;
-    if (A.trace)
+    if (tracing)
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tr_claim));
     __syncwarp();
 #if SFG_ML1_UNROLL
@@ -659,7 +667,7 @@ __global__ void __launch_bounds__(kMThreads) k_mline1(const MLineArgs A) {
 #pragma unroll 1
 #endif
     for (int i = -kRA1; i < T; ++i) {
-      if (A.trace && i == 0)
+      if (tracing && i == 0)
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tr_first));
       // commit groups <= i - kXA1 complete: records of steps <= i + kXA1,
       // gathers of steps <= i
@@ -667,7 +675,7 @@ __global__ void __launch_bounds__(kMThreads) k_mline1(const MLineArgs A) {
       __syncwarp();
       // ---- record of step i+kRA1
       if (i + kRA1 < T) {
-        const int q = (i + kRA1) % kQ1;
+        const int q = (i + kRA1) & (kQ1 - 1);
         const int64_t rec = base + (int64_t)(i + kRA1) * 32;
         const double* vr = sval + rec * (CH + 4);
 #pragma unroll
@@ -681,7 +689,7 @@ __global__ void __launch_bounds__(kMThreads) k_mline1(const MLineArgs A) {
       }
       // ---- right-hand side and external words of step i+kXA1
       if (i + kXA1 >= 0 && i + kXA1 < T) {
-        const int q = (i + kXA1) % kQ1, qx = (i + kXA1) % kX1;
+        const int q = (i + kXA1) & (kQ1 - 1), qx = (i + kXA1) & (kX1 - 1);
         const int r = W.row[q][lane];
         if (r >= 0) {
           cp8(&W.rhs[qx][lane], rhs_vec + r);
@@ -695,9 +703,9 @@ __global__ void __launch_bounds__(kMThreads) k_mline1(const MLineArgs A) {
       }
       asm volatile("cp.async.commit_group;" ::: "memory");
       // ---- row of step i
-      const long long dc0 = A.trace ? clock64() : 0;
+      const long long dc0 = tracing ? clock64() : 0;
       if (i >= 0) {
-        const int q = i % kQ1, qx = i % kX1;
+        const int q = i & (kQ1 - 1), qx = i & (kX1 - 1);
         const int r = W.row[q][lane];
         if (r >= 0) {
           const double d = W.v[q][lane][CH + 1];
@@ -717,7 +725,7 @@ __global__ void __launch_bounds__(kMThreads) k_mline1(const MLineArgs A) {
                   W.ring[(i - (t >> 5)) & (kRing - 1)][t & 31]);
             }
           }
-          const long long pc0 = A.trace ? clock64() : 0;
+          const long long pc0 = tracing ? clock64() : 0;
           for (;;) {
             bool pending = is_sent_hi(rw);
 #pragma unroll
@@ -732,7 +740,7 @@ __global__ void __launch_bounds__(kMThreads) k_mline1(const MLineArgs A) {
               if (is_sent_hi(wd[a]))
                 wd[a] = ld_relaxed_u64(xo + cds[a]);
           }
-          if (A.trace)
+          if (tracing)
             poll_cyc += clock64() - pc0;
           double acc = __longlong_as_double((long long)rw);
 #pragma unroll
@@ -750,12 +758,12 @@ __global__ void __launch_bounds__(kMThreads) k_mline1(const MLineArgs A) {
         }
       }
       __syncwarp();
-      if (A.trace)
+      if (tracing)
         d_cyc += clock64() - dc0;
     }
     asm volatile("cp.async.wait_group 0;" ::: "memory");
     __syncwarp();
-    if (A.trace) {
+    if (tracing) {
       unsigned long long pm = poll_cyc;
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) {

@@ -1,4 +1,6 @@
-"""Timeline of the multi-chain executor (SFG_TRACE diagnostics): group
+"""(k_mline1 records its timeline only in a build with -DSFG_ML1_TRACE=1:
+bash scripts/build_alt.sh ml1trace "-DSFG_ML1_TRACE=1", then SFG_LIB=old_lib/ml1trace/libsfgpu.so.)
+Timeline of the multi-chain executor (SFG_TRACE diagnostics): group
 durations, step times and where the steps stall."""
 import os, sys, json
 import numpy as np

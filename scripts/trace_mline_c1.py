@@ -1,4 +1,6 @@
-"""Multi-line executor timeline on the C1 matrix (one forward solve pair)."""
+"""(k_mline1 records its timeline only in a build with -DSFG_ML1_TRACE=1:
+bash scripts/build_alt.sh ml1trace "-DSFG_ML1_TRACE=1", then SFG_LIB=old_lib/ml1trace/libsfgpu.so.)
+Multi-line executor timeline on the C1 matrix (one forward solve pair)."""
 import os, sys
 import numpy as np
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
