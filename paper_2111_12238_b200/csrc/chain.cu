@@ -16,6 +16,16 @@
 #define SFG_CHAIN_THREADS 384
 #endif
 
+#ifndef SFG_CHAIN_TRACE
+// 1: the chain kernels record their tile timeline when SFG_TRACE is set
+// (diagnostic builds: scripts/build_alt.sh trace "-DSFG_CHAIN_TRACE=1")
+#define SFG_CHAIN_TRACE 0
+#endif
+
+#ifndef SFG_CHAIN_UNROLL
+#define SFG_CHAIN_UNROLL 1 // unroll factor of k_chain_sm's tile loop (2: 2.42 ms, 3: 2.48 ms against 1.93 ms on C5)
+#endif
+
 #ifndef SFG_REFRESH
 #define SFG_REFRESH 1 // re-stage a tile's dependency words before stage C (0: off, A/B builds)
 #endif
@@ -367,7 +377,8 @@ __global__ void __launch_bounds__(kThreads) k_chain(const ChainArgs A) {
     const double* xs = pass1 ? xo : A.vout;
     const double* rs = pass1 ? rhs_vec : A.vmid;
     const bool rpoll = pass1 ? bwd : true;
-    unsigned long long* tr = A.trace ? A.trace + (size_t)item * A.trace_tiles * 3 : nullptr;
+    unsigned long long* tr =
+        SFG_CHAIN_TRACE && A.trace ? A.trace + (size_t)item * A.trace_tiles * 3 : nullptr;
     const unsigned long long t_claim = tr ? gtimer() : 0ull;
     if (solve) {
       auto row_of = [&](int o) { const int p = p0 + o; return bwd ? A.n - 1 - p : p; };
@@ -614,7 +625,8 @@ __global__ void __launch_bounds__(kSmThreads, COMBO == 1 ? 1 : SFG_CHAIN_MINB) k
     const double* xs = pass1 ? xo : A.vout;
     const double* rs = pass1 ? rhs_vec : A.vmid;
     const bool rpoll = pass1 ? bwd : true;
-    unsigned long long* tr = A.trace ? A.trace + (size_t)item * A.trace_tiles * 3 : nullptr;
+    unsigned long long* tr =
+        SFG_CHAIN_TRACE && A.trace ? A.trace + (size_t)item * A.trace_tiles * 3 : nullptr;
     const unsigned long long t_claim = tr ? gtimer() : 0ull;
     auto row_of = [&](int o) { const int p = p0 + o; return bwd ? A.n - 1 - p : p; };
     auto active = [&](int tile) {
@@ -673,7 +685,12 @@ __global__ void __launch_bounds__(kSmThreads, COMBO == 1 ? 1 : SFG_CHAIN_MINB) k
       }
     }
     __syncwarp();
+#if SFG_CHAIN_UNROLL > 1
+    constexpr int kUnrollT = SFG_CHAIN_UNROLL;
+#pragma unroll kUnrollT
+#else
 #pragma unroll 1
+#endif
     for (int t = -3; t < ntiles; ++t) {
       // stage A: row pointers of tile t+3
       int npb = 0, npe = 0;

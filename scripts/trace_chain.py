@@ -1,4 +1,6 @@
-"""Runs one traced execution of a config on the GPU and summarises the
+"""(The chain kernels record their timeline only in a build with -DSFG_CHAIN_TRACE=1:
+bash scripts/build_alt.sh trace "-DSFG_CHAIN_TRACE=1", then SFG_LIB=old_lib/trace/libsfgpu.so.)
+Runs one traced execution of a config on the GPU and summarises the
 chain executor's timeline (diagnostics; SFG_TRACE)."""
 import os, sys, json
 import numpy as np

@@ -1,4 +1,6 @@
-"""Cycle-level split of the chain executor's tiles (S >= 2 kernel):
+"""(The chain kernels record their timeline only in a build with -DSFG_CHAIN_TRACE=1:
+bash scripts/build_alt.sh trace "-DSFG_CHAIN_TRACE=1", then SFG_LIB=old_lib/trace/libsfgpu.so.)
+Cycle-level split of the chain executor's tiles (S >= 2 kernel):
 wait phase (cp.async wait + polls + sums) and carry phase, per tile."""
 import os, sys, json
 import numpy as np

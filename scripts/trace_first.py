@@ -1,4 +1,6 @@
-"""C5 chain executor: where a level's lag goes, first tile vs a middle tile.
+"""(The chain kernels record their timeline only in a build with -DSFG_CHAIN_TRACE=1:
+bash scripts/build_alt.sh trace "-DSFG_CHAIN_TRACE=1", then SFG_LIB=old_lib/trace/libsfgpu.so.)
+C5 chain executor: where a level's lag goes, first tile vs a middle tile.
 For every forward chain (27-point grid line (y, z)) and tile t in {0, 16}:
   hop   = consumer 'all words summed' - latest producer tile end it needs
   after = consumer tile end - consumer 'all words summed' (the carry)

@@ -1,4 +1,6 @@
-"""Effective hop inside the C5 chain executor (forward solve, natural-order
+"""(The chain kernels record their timeline only in a build with -DSFG_CHAIN_TRACE=1:
+bash scripts/build_alt.sh trace "-DSFG_CHAIN_TRACE=1", then SFG_LIB=old_lib/trace/libsfgpu.so.)
+Effective hop inside the C5 chain executor (forward solve, natural-order
 27-point grid): for every tile, the time from the last producer tile it
 depends on ending to the consumer having summed all its terms.
 Chain c is grid line (y, z) = (c % N, c // N)."""

@@ -1,4 +1,6 @@
-"""Per-level timing of the C5 chain executor from SFG_TRACE: tile-end times
+"""(The chain kernels record their timeline only in a build with -DSFG_CHAIN_TRACE=1:
+bash scripts/build_alt.sh trace "-DSFG_CHAIN_TRACE=1", then SFG_LIB=old_lib/trace/libsfgpu.so.)
+Per-level timing of the C5 chain executor from SFG_TRACE: tile-end times
 (globaltimer) per chain level, the per-level lag and the in-chain tile period."""
 import os, sys
 import numpy as np
