@@ -14,6 +14,12 @@
 #include "common.cuh"
 #include "fact.cuh"
 
+#ifndef SFG_FACT_TRACE
+// 1: the warp executors record their task timeline when SFG_TRACE is set
+// (diagnostic builds: scripts/build_alt.sh trace "-DSFG_FACT_TRACE=1")
+#define SFG_FACT_TRACE 0
+#endif
+
 #ifndef SFG_IC_BUNROLL
 #define SFG_IC_BUNROLL 0 // unroll factor of the IC0 update-batch loop (2: C4 9.19 -> 9.63 ms)
 #endif
@@ -271,7 +277,8 @@ __global__ void __launch_bounds__(kFBlock, COMBO == 5 ? SFG_IC5_MINB : SFG_IC7_M
     const int m = c1_nx - c0;
     const int q0 = q0_nx;
     const int q1 = q1_nx;
-    unsigned long long* const ftr = A.ftrace ? A.ftrace + (size_t)c * 5 : nullptr;
+    unsigned long long* const ftr =
+        SFG_FACT_TRACE && A.ftrace ? A.ftrace + (size_t)c * 5 : nullptr;
     if (ftr && lane == 0) {
       ftr[0] = (unsigned long long)k;
       ftr[1] = ftimer();
@@ -683,7 +690,8 @@ __global__ void __launch_bounds__(kFBlock, MAXU <= 4 ? SFG_ILU_MINB4 : 1) k_ilu0
     const int i = i_nx;
     const int r0 = r0_nx;
     const int m = r1_nx - r0;
-    unsigned long long* const ftr = A.ftrace ? A.ftrace + (size_t)c * 5 : nullptr;
+    unsigned long long* const ftr =
+        SFG_FACT_TRACE && A.ftrace ? A.ftrace + (size_t)c * 5 : nullptr;
     if (ftr && lane == 0) {
       ftr[0] = (unsigned long long)i;
       ftr[1] = ftimer();

@@ -1,4 +1,6 @@
-"""Per-level timing of the factorization warp executors (configs 2, 3, 4)
+"""(The warp executors record their timeline only in a build with -DSFG_FACT_TRACE=1:
+bash scripts/build_alt.sh trace "-DSFG_FACT_TRACE=1", then SFG_LIB=old_lib/trace/libsfgpu.so.)
+Per-level timing of the factorization warp executors (configs 2, 3, 4)
 from SFG_TRACE: per task {start, summed, factor published, solve published}."""
 import os, sys
 import numpy as np
