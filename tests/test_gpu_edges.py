@@ -1,7 +1,8 @@
 """Edge cases through the C-ABI, every executor, bit-exact against the oracle:
 empty and 1x1 systems, diagonal-only matrices (no dependencies, every chain
 of length 1), dense blocks (rows far wider than any staging width, so the
-long-row paths run), a single long chain (bidiagonal), and isolated rows."""
+long-row paths run), a single long chain (bidiagonal), isolated rows, and an arrow matrix (two-entry
+columns under one dense row)."""
 import numpy as np
 import pytest
 
@@ -38,7 +39,19 @@ def spd(n, bw, seed):
     return D
 
 
+def arrow(n, seed):
+    """Diagonal plus a dense last row/column: every column has two entries
+    (the warp executors take it) while the last row has n-1 lower entries, so
+    the fused IC0 kernel's solve row runs over several 32-term chunks."""
+    rng = np.random.default_rng(seed)
+    D = np.diag(rng.uniform(2.0, 3.0, n))
+    D[n - 1, :n - 1] = D[:n - 1, n - 1] = -rng.uniform(0.01, 0.02, n - 1)
+    D[n - 1, n - 1] = 4.0
+    return D
+
+
 CASES = {
+    "arrow": arrow(100, 4),
     "n1": np.array([[3.0]]),
     "diag": np.diag(np.arange(1.0, 40.0)),
     "bidiag": np.eye(300) * 4 - np.eye(300, k=-1) - np.eye(300, k=1),
